@@ -1,0 +1,87 @@
+// vdmc_internal.cuh -- shared declarations of libvdmc.so (product path; no oracle code here).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <cuda_runtime.h>
+
+#include "../../include/vdmc.h"
+
+namespace vdmc {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+vdmc_status fail(vdmc_status st, const char *fmt, ...);
+void count_launch(int n = 1);
+
+#define VDMC_CUDA(call)                                                                  \
+    do {                                                                                 \
+        cudaError_t err_ = (call);                                                       \
+        if (err_ != cudaSuccess)                                                         \
+            return ::vdmc::fail(err_ == cudaErrorMemoryAllocation ? VDMC_ENOMEM : VDMC_ECUDA, \
+                                "%s:%d %s: %s", __FILE__, __LINE__, #call,               \
+                                cudaGetErrorString(err_));                               \
+    } while (0)
+
+#define VDMC_LAUNCH()                                                                    \
+    do {                                                                                 \
+        ::vdmc::count_launch();                                                          \
+        cudaError_t err_ = cudaGetLastError();                                           \
+        if (err_ != cudaSuccess)                                                         \
+            return ::vdmc::fail(VDMC_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__,      \
+                                cudaGetErrorString(err_));                               \
+    } while (0)
+
+// --------------------------------------------------------- motif classes
+// Device mask layout ("pair-code-major", any bijection of the paper's index is allowed,
+// SURVEY §8(a) S3): vertices in enumeration order (r, a, b, c); pair p of (0,1),(0,2),(0,3),
+// (1,2),(1,3),(2,3) [k=4] or (0,1),(0,2),(1,2) [k=3] occupies bits 2p..2p+1 with
+//   bit 2p   = first -> second,   bit 2p+1 = second -> first.
+// The host LUT maps every such mask to the column of its minimum-isomorph paper index.
+constexpr int kNumClasses3 = 13;
+constexpr int kNumClasses4 = 199;
+constexpr uint8_t kNoClass = 255;
+
+const uint8_t *host_lut(int k);          // [64] or [4096]
+const uint16_t *host_class_ids(int k);   // [13] or [199]
+int num_classes(int k);
+
+}  // namespace vdmc
+
+// ------------------------------------------------------------ graph handle
+struct vdmc_graph {
+    int device = 0;
+    int64_t n = 0, nnz = 0, arcs = 0, ntasks = 0, max_degree = 0;
+    // G_U in rank order.  adj entry = (rank(nbr) << 2) | code, code bit0 = owner -> nbr,
+    // bit1 = nbr -> owner; every list sorted ascending (= by rank).
+    int64_t *off = nullptr;        // [n+1]
+    int64_t *split = nullptr;      // [n]   first entry of v's list with rank > v
+    uint32_t *adj = nullptr;       // [nnz]
+    int32_t *order = nullptr;      // [n]   order[rank] = original id
+    int64_t *tfirst = nullptr;     // [n+1] first task of each root (exclusive scan of forward degrees)
+    int32_t *task_root = nullptr;  // [ntasks]
+    // scratch owned by the handle (lazily grown)
+    uint64_t *acc = nullptr;       // [n][C] accumulator in rank order
+    size_t acc_bytes = 0;
+    uint32_t *lscratch = nullptr;  // per-warp depth-2 candidate lists
+    size_t lscratch_elems = 0;
+    unsigned long long *ctr = nullptr;   // work counter(s)
+    uint8_t *lut3 = nullptr, *lut4 = nullptr;
+    int64_t *cost = nullptr;       // [ntasks] inclusive prefix of the plan's cost proxy
+    int cost_k = 0;
+    // profiling
+    int profiling = 0;
+    cudaEvent_t ev[8] = {};
+    float last_ms[5] = {0, 0, 0, 0, 0};
+    float build_ms = 0;
+};
+
+namespace vdmc {
+vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst,
+                         const int32_t *h_rank, int device, cudaStream_t stream, vdmc_graph *g);
+vdmc_status ensure_acc(vdmc_graph *g, int k);
+vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t stream);
+vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi,
+                         cudaStream_t stream);
+}  // namespace vdmc

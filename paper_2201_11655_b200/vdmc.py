@@ -1,0 +1,243 @@
+"""Thin ctypes binding over libvdmc.so (include/vdmc.h).  Argument marshalling only:
+every step of the counting path runs in the library's CUDA kernels.  PyTorch supplies
+device memory, streams and process groups.  There is no CPU fallback: if the library or a
+CUDA device is missing, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libvdmc.so")
+
+VDMC_OK = 0
+STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASYM",
+          5: "VDMC_EORDER", 6: "VDMC_EK", 7: "VDMC_ENOMEM", 8: "VDMC_ECUDA", 9: "VDMC_ENODEV"}
+
+# Every symbol include/vdmc.h declares (tests check the .so exports exactly these)
+EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_count", "vdmc_plan",
+           "vdmc_split_costs", "vdmc_num_classes", "vdmc_class_ids", "vdmc_get_info",
+           "vdmc_get_order", "vdmc_set_profiling", "vdmc_last_timings",
+           "vdmc_kernel_launches", "vdmc_free_graph", "vdmc_last_error"]
+
+
+class VdmcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class Range(ctypes.Structure):
+    _fields_ = [("task_lo", ctypes.c_int64), ("task_hi", ctypes.c_int64)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("arcs", ctypes.c_int64),
+                ("ntasks", ctypes.c_int64), ("max_degree", ctypes.c_int64), ("device", ctypes.c_int32)]
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+def lib():
+    """Load libvdmc.so (built by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libvdmc.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        sig = {
+            "vdmc_build_graph_edges": (_i32, [_i64, _i64, _vp, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp,
+                                              ctypes.POINTER(_vp)]),
+            "vdmc_build_graph": (_i32, [_i64, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)]),
+            "vdmc_count": (_i32, [_vp, ctypes.c_int, _vp, ctypes.POINTER(Range), _vp]),
+            "vdmc_plan": (_i32, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Range)]),
+            "vdmc_split_costs": (_i32, [_vp, _i64, ctypes.c_int, ctypes.POINTER(Range)]),
+            "vdmc_num_classes": (ctypes.c_int, [ctypes.c_int]),
+            "vdmc_class_ids": (_i32, [ctypes.c_int, _vp]),
+            "vdmc_get_info": (_i32, [_vp, ctypes.POINTER(Info)]),
+            "vdmc_get_order": (_i32, [_vp, _vp]),
+            "vdmc_set_profiling": (_i32, [_vp, ctypes.c_int]),
+            "vdmc_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
+            "vdmc_kernel_launches": (_i64, []),
+            "vdmc_free_graph": (None, [_vp]),
+            "vdmc_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != VDMC_OK:
+        raise VdmcError(st, lib().vdmc_last_error().decode())
+
+
+def num_classes(k: int) -> int:
+    return lib().vdmc_num_classes(k)
+
+
+def class_ids(k: int) -> np.ndarray:
+    C = num_classes(k)
+    if C < 0:
+        _check(lib().vdmc_class_ids(k, None))
+    out = np.zeros(C, np.uint16)
+    _check(lib().vdmc_class_ids(k, out.ctypes.data))
+    return out
+
+
+def split_costs(prefix: np.ndarray, nparts: int):
+    prefix = np.ascontiguousarray(prefix, dtype=np.int64)
+    parts = (Range * nparts)()
+    _check(lib().vdmc_split_costs(prefix.ctypes.data if prefix.size else None, prefix.size, nparts, parts))
+    return [(p.task_lo, p.task_hi) for p in parts]
+
+
+def kernel_launches() -> int:
+    return int(lib().vdmc_kernel_launches())
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Graph:
+    """A graph resident on one GPU (vdmc_graph).  Build from a directed edge list."""
+
+    def __init__(self, n: int, src, dst, rank=None, device: int = 0, stream=None):
+        import torch
+        self._h = _vp()
+        rk = None
+        if rank is not None:
+            rk = np.ascontiguousarray(rank, dtype=np.int32)
+        if isinstance(src, torch.Tensor) and src.is_cuda:
+            assert src.dtype == torch.int32 and dst.dtype == torch.int32
+            src, dst = src.contiguous(), dst.contiguous()
+            device = src.device.index
+            with torch.cuda.device(device):
+                st = lib().vdmc_build_graph_edges(n, src.numel(), src.data_ptr(), dst.data_ptr(), 1,
+                                                  rk.ctypes.data if rk is not None else None, device,
+                                                  _stream_ptr(stream), ctypes.byref(self._h))
+        else:
+            s = np.ascontiguousarray(src, dtype=np.int32)
+            d = np.ascontiguousarray(dst, dtype=np.int32)
+            with torch.cuda.device(device):
+                st = lib().vdmc_build_graph_edges(n, s.size, s.ctypes.data if s.size else None,
+                                                  d.ctypes.data if d.size else None, 0,
+                                                  rk.ctypes.data if rk is not None else None, device,
+                                                  _stream_ptr(stream), ctypes.byref(self._h))
+        _check(st)
+        self.device = device
+        self.info = self._info()
+
+    @classmethod
+    def from_sym_csr(cls, n: int, indptr, nbr, dirc, rank=None, device: int = 0) -> "Graph":
+        """Build from the symmetric G_U CSR + direction codes (vdmc_build_graph)."""
+        self = cls.__new__(cls)
+        self._h = _vp()
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        nb = np.ascontiguousarray(nbr, dtype=np.int32)
+        dc = np.ascontiguousarray(dirc, dtype=np.uint8)
+        rk = None if rank is None else np.ascontiguousarray(rank, dtype=np.int32)
+        _check(lib().vdmc_build_graph(n, ip.ctypes.data, nb.ctypes.data if nb.size else None,
+                                      dc.ctypes.data if dc.size else None,
+                                      rk.ctypes.data if rk is not None else None, device, ctypes.byref(self._h)))
+        self.device = device
+        self.info = self._info()
+        return self
+
+    def _info(self) -> dict:
+        inf = Info()
+        _check(lib().vdmc_get_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in Info._fields_}
+
+    @property
+    def n(self) -> int:
+        return self.info["n"]
+
+    @property
+    def ntasks(self) -> int:
+        return self.info["ntasks"]
+
+    def order(self) -> np.ndarray:
+        out = np.zeros(max(self.n, 1), np.int32)
+        _check(lib().vdmc_get_order(self._h, out.ctypes.data))
+        return out[: self.n]
+
+    def count(self, k: int, out=None, work=None, stream=None):
+        """uint64 counts [n][C] as an int64 torch tensor on the graph's device (same bits)."""
+        import torch
+        C = num_classes(k)
+        if C < 0:
+            _check(lib().vdmc_count(self._h, k, None, None, None))
+        if out is None:
+            out = torch.empty((self.n, C), dtype=torch.int64, device=f"cuda:{self.device}")
+        assert out.is_cuda and out.dtype == torch.int64 and out.is_contiguous() and out.shape == (self.n, C)
+        rng = None
+        if work is not None:
+            rng = Range(int(work[0]), int(work[1]))
+        with torch.cuda.device(self.device):
+            _check(lib().vdmc_count(self._h, k, out.data_ptr() if out.numel() else None,
+                                    ctypes.byref(rng) if rng is not None else None, _stream_ptr(stream)))
+        return out
+
+    def plan(self, k: int, nparts: int):
+        parts = (Range * nparts)()
+        _check(lib().vdmc_plan(self._h, k, nparts, parts))
+        return [(p.task_lo, p.task_hi) for p in parts]
+
+    def set_profiling(self, on: bool = True):
+        _check(lib().vdmc_set_profiling(self._h, 1 if on else 0))
+
+    def timings(self) -> dict:
+        ms = (ctypes.c_float * 5)()
+        _check(lib().vdmc_last_timings(self._h, ms, 5))
+        return dict(zip(["build", "plan", "enum", "finalize", "count"], list(ms)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().vdmc_free_graph(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def count(n: int, src, dst, k: int, device: int = 0, rank=None):
+    """One-shot: build the graph on `device`, count k-motifs, return a host uint64 [n][C]."""
+    g = Graph(n, src, dst, rank=rank, device=device)
+    try:
+        out = g.count(k)
+        return out.cpu().numpy().view(np.uint64)
+    finally:
+        g.close()
+
+
+def count_distributed(g: Graph, k: int, group=None, dst_rank: int = 0):
+    """Multi-GPU: the graph is replicated on every rank; rank p counts the
+    p-th cost-balanced slice of the (root, neighbour) task list into a private partial; one
+    NCCL reduce (sum over int64 = the same bits as uint64 wrap-around addition) gives the full
+    matrix on dst_rank.  Returns the reduced tensor on dst_rank, the local partial elsewhere."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    parts = g.plan(k, world)
+    out = g.count(k, work=parts[me])
+    dist.reduce(out, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
+    return out
