@@ -4,36 +4,49 @@
 // The method: for every root r, count the proper k-BFS(r) -- the connected
 // k-sets whose lowest-index vertex is r (Lemma 1) -- grouped by BFS-level shape
 // (Lemma 2), each set once (Lemma 3; Lemma 4).  In rank order
-// (vertex id = rank) with N+(x) = {u in N(x) : u > r} and L_x = N+(x) \ N(r) (depth-2
-// children of depth-1 vertex x), the S-local shape rules (reading G4/G5) are
-//   k = 3:  "2"     a < b in N+(r)
-//           "1+1"   a in N+(r), b in L_a
-//   k = 4:  "3"     a < b < c in N+(r)
-//           "2+1"   a < b in N+(r), c in L_a, or c in L_b \ N(a)
-//           "1+2"   a in N+(r), b < c in L_a
-//           "1+1+1" a in N+(r), b in L_a, c in N+(b) \ N(r) \ N(a)
-// Every connected set with minimum r falls in exactly one case once (its depth-1 set
-// S n N(r) has 3, 2 or 1 members).
+// (vertex id = rank) with R = N+(r) = {u in N(r) : u > r} and L_x = N+(x) \ N(r) (the
+// depth-2 children of a depth-1 vertex x), the S-local shape rules (readings G4/G5) are
+//   k = 3:  "2"     a < b in R
+//           "1+1"   a in R, b in L_a
+//   k = 4:  "3"     a < b < c in R
+//           "2+1"   a < b in R, c in L_a, or c in L_b \ N(a)
+//           "1+2"   a in R, b < c in L_a
+//           "1+1+1" a in R, b in L_a, c in N+(b) \ N(r) \ N(a)   (Lemma 4: c may be "depth 2")
+// Every connected set with minimum r falls in exactly one case, once.
 //
-// Work unit: the task (r, a), a in N+(r): one warp; lanes split the inner loops.
-// Classification: the pair codes of (r, a, b, c) form a 12-bit (6-bit) mask
-// -> shared-memory LUT -> column of the minimum-isomorph class ("in real time").
-// Accumulation ("for each vertex"; P:334 atomic add): r and a are fixed per task and
-// share one per-warp shared-memory histogram (flushed once per task); b is warp-uniform in
-// every inner loop, so equal columns are merged with __match_any_sync and added once; the
-// innermost member c (k = 4) or b (k = 3) takes one u64 atomicAdd per set.
+// Work unit ("each pair of a vertex and one of its neighbors"): the task (r, a).
+//   * heavy roots (deg(r) > kLightDeg): one CTA per task; the 16 warps split the loops over
+//     b.  R and L_a live in shared memory (global scratch if the graph's degree is too big).
+//   * light roots: one warp per root, its tasks in sequence; R and L_a in the warp's smem.
+//   One persistent kernel: CTAs drain the heavy task list (ordered by rank = degree
+//   descending, then by a's position: longest first), then their warps drain the light
+//   roots.  Both lists come from a global atomic counter.
+// Membership tests are binary searches in the staged sorted lists (shared memory).  The
+// codes (a, x) and (b, x) for x in R or L_a are scattered once into 2-bit-per-position
+// bitmaps, so the innermost loops (one set per lane) read only shared memory.
+// Classification: the pair codes of (r, a, b, c) form a 12-bit (6-bit) mask ->
+// shared-memory LUT -> column of the minimum-isomorph class, "in real time".
+// Accumulation (P:334 atomic add): r and a are fixed per task: one warp-private u32
+// histogram, flushed per task into rows r and a; b is warp-uniform in every inner loop
+// (k = 4): lanes with equal columns are merged by __match_any_sync into one atomic; the
+// innermost member (c for k = 4, b for k = 3) takes one u64 atomicAdd per set.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "vdmc_internal.cuh"
 
 namespace vdmc {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 16;            // warps per CTA
 constexpr int kBlock = kWarps * 32;
+constexpr int kLightDeg = 256;        // light root: G_U degree <= this
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNone = 255;
 
 struct Dev {
     const int64_t *__restrict__ off;
@@ -41,215 +54,353 @@ struct Dev {
     const uint32_t *__restrict__ adj;
     const int64_t *__restrict__ tfirst;
     const int32_t *__restrict__ task_root;
-    unsigned long long *__restrict__ acc;   // [n][C], row = rank
+    const int32_t *__restrict__ heavy_task;   // task ids of heavy roots, rank order
+    const int32_t *__restrict__ light_root;   // light roots, rank order
+    int64_t nheavy, nlight;
+    unsigned long long *__restrict__ acc;     // [n][C], row = rank
+    uint32_t *__restrict__ gheavy;            // global fallback: per-CTA heavy buffers
+    uint32_t *__restrict__ glight;            // global fallback: per-warp oversize L_a + bitmap
+    int64_t gheavy_per_cta, glight_per_warp;  // words
+    int heavy_in_smem;                        // heavy buffers fit in shared memory
+    int big;                                  // degrees so large a task could overflow u32 histograms
+    int maxdeg;
 };
 
-__device__ __forceinline__ uint32_t swap2(uint32_t c) { return ((c & 1u) << 1) | (c >> 1); }
+// shared-memory layout (words), computed on the host
+struct Layout {
+    int R, La, Ba, Bb, Bl;        // heavy: R[maxdeg], La[maxdeg], Ba[bw], Bb[kWarps][bw], Bl[kWarps][lw]
+    int bw, lw;                   // bitmap words for R positions / L positions
+    int hist;                     // per-warp u32 histograms [kWarps][C]
+    int light;                    // light region: per warp kLightWords
+    int total;                    // words
+};
+constexpr int kLW = kLightDeg;               // light list capacity
+constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
+// per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
+constexpr int kLightWords = 2 * kLW + 3 * kLB;
 
-// first position in [lo, hi) whose entry has rank >= key (entries sort like their rank)
-__device__ __forceinline__ int64_t lower_rank(const uint32_t *__restrict__ adj, int64_t lo, int64_t hi,
-                                              uint32_t key) {
-    const uint32_t k2 = key << 2;
+__device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x) {
+    // position of vertex x in the sorted entry list S[0..len), or -1
+    const uint32_t key = x << 2;
+    int lo = 0, hi = len;
     while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (__ldg(adj + mid) < k2) lo = mid + 1;
+        const int mid = (lo + hi) >> 1;
+        if (S[mid] < key) lo = mid + 1;
         else hi = mid;
     }
-    return lo;
+    return (lo < len && (S[lo] >> 2) == x) ? lo : -1;
 }
 
-// code of y in the list [lo, hi) (owner's perspective), 0 if absent
-__device__ __forceinline__ uint32_t code_in(const uint32_t *__restrict__ adj, int64_t lo, int64_t hi, uint32_t y) {
-    int64_t p = lower_rank(adj, lo, hi, y);
-    if (p < hi) {
-        uint32_t e = __ldg(adj + p);
-        if ((e >> 2) == y) return e & 3u;
-    }
-    return 0;
+__device__ __forceinline__ uint32_t get2(const uint32_t *B, int p) { return (B[p >> 4] >> ((p & 15) << 1)) & 3u; }
+__device__ __forceinline__ void set2(uint32_t *B, int p, uint32_t code) { atomicOr(B + (p >> 4), code << ((p & 15) << 1)); }
+
+template <int NW>
+__device__ __forceinline__ void team_sync() {
+    if constexpr (NW == 1) __syncwarp();
+    else __syncthreads();
 }
 
-// code(x, y): bit0 = x -> y, bit1 = y -> x; searched in the shorter list
-__device__ __forceinline__ uint32_t pair_code(const Dev &g, uint32_t x, uint32_t y) {
-    const int64_t x0 = __ldg(g.off + x), x1 = __ldg(g.off + x + 1);
-    const int64_t y0 = __ldg(g.off + y), y1 = __ldg(g.off + y + 1);
-    if (x1 - x0 <= y1 - y0) return code_in(g.adj, x0, x1, y);
-    return swap2(code_in(g.adj, y0, y1, x));
-}
-
-// r and a of the task: +cnt per column group in the warp's histogram
-__device__ __forceinline__ void add_root(unsigned long long *wcnt, int col, int lane) {
-    const unsigned m = __match_any_sync(kFull, col);
-    if (col != kNoClass && lane == __ffs(m) - 1) wcnt[col] += __popc(m);
-}
-
-// r, a (histogram) and the warp-uniform member b (one atomic per column group)
+// one set with members r, a (histogram H), b (warp-uniform, merged per column) and c (lane)
 template <int C>
-__device__ __forceinline__ void add_root_b(unsigned long long *wcnt, unsigned long long *acc, uint32_t b, int col,
-                                           int lane) {
+__device__ __forceinline__ void emit4(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t b, uint32_t c,
+                                      int col, int lane) {
+    if (col != kNone) atomicAdd(acc + (size_t)c * C + col, 1ull);
     const unsigned m = __match_any_sync(kFull, col);
-    if (col != kNoClass && lane == __ffs(m) - 1) {
+    if (col != kNone && lane == __ffs(m) - 1) {
         const unsigned cnt = __popc(m);
-        wcnt[col] += cnt;
+        H[col] += cnt;
         atomicAdd(acc + (size_t)b * C + col, (unsigned long long)cnt);
     }
 }
 
+// one set with members r, a (histogram H) and b (lane)
+template <int C>
+__device__ __forceinline__ void emit3(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t b, int col,
+                                      int lane) {
+    if (col != kNone) atomicAdd(acc + (size_t)b * C + col, 1ull);
+    const unsigned m = __match_any_sync(kFull, col);
+    if (col != kNone && lane == __ffs(m) - 1) H[col] += __popc(m);
+}
+
+// warp-private histogram -> rows r and a
+template <int C>
+__device__ __forceinline__ void flush_hist(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t r, uint32_t a,
+                                           int lane) {
+    __syncwarp();
+    for (int j = lane; j < C; j += 32) {
+        const uint32_t v = H[j];
+        if (v) {
+            atomicAdd(acc + (size_t)r * C + j, (unsigned long long)v);
+            atomicAdd(acc + (size_t)a * C + j, (unsigned long long)v);
+            H[j] = 0;
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void clear_words(uint32_t *B, int w0, int w1, int lane) {   // words [w0, w1)
+    for (int w = w0 + lane; w < w1; w += 32) B[w] = 0;
+}
+
+// Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
+// Run by one warp.  Returns |L_a|.
+__device__ int build_a(const Dev &g, uint32_t r, uint32_t a, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
+                       int lane) {
+    const int64_t a0 = g.off[a], a1 = g.off[a + 1];
+    int nL = 0;
+    for (int64_t base = a0; base < a1; base += 32) {
+        const int64_t p = base + lane;
+        bool keep = false;
+        uint32_t e = 0;
+        if (p < a1) {
+            e = g.adj[p];
+            const uint32_t x = e >> 2;
+            if (x > r) {
+                const int pos = find_rank(R, D, x);
+                if (pos >= 0) set2(Ba, pos, e & 3u);
+                else keep = true;
+            }
+        }
+        const unsigned bal = __ballot_sync(kFull, keep);
+        if (keep) La[nL + __popc(bal & ((1u << lane) - 1u))] = e;
+        nL += __popc(bal);
+    }
+    __syncwarp();
+    return nL;
+}
+
+// The task (r, a = R[i]) for a team of NW warps (warp w of the team).  Ba/La must be built
+// (phase A) and visible to the team.  Bb/Bl are this warp's scratch bitmaps (all zero on
+// entry and exit).  H is this warp's histogram.
+template <int K, int NW>
+__device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
+                           const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb, uint32_t *Bl, uint32_t *H,
+                           int w, int lane) {
+    constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
+    unsigned long long *__restrict__ acc = g.acc;
+    const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
+    if constexpr (K == 3) {
+        // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
+        for (int base = i + 1 + w * 32; base < D; base += NW * 32) {
+            const int p = base + lane;
+            int col = kNone;
+            uint32_t b = 0;
+            if (p < D) {
+                const uint32_t eb = R[p];
+                b = eb >> 2;
+                col = lut[cra | (eb & 3u) << 2 | get2(Ba, p) << 4];
+            }
+            emit3<C>(H, acc, b, col, lane);
+        }
+        // "1+1": b in L_a.   (r,b) = 0
+        for (int base = w * 32; base < nL; base += NW * 32) {
+            const int q = base + lane;
+            int col = kNone;
+            uint32_t b = 0;
+            if (q < nL) {
+                const uint32_t eb = La[q];
+                b = eb >> 2;
+                col = lut[cra | (eb & 3u) << 4];
+            }
+            emit3<C>(H, acc, b, col, lane);
+        }
+        if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    } else {
+        // mask: (r,a) | (r,b)<<2 | (r,c)<<4 | (a,b)<<6 | (a,c)<<8 | (b,c)<<10
+        for (int j = i + 1 + w; j < D; j += NW) {                // b = R[j]
+            const uint32_t eb = R[j], b = eb >> 2;
+            const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
+            const int64_t b0 = g.off[b], b1 = g.off[b + 1];
+            // walk N(b): c in R after b -> Bb;  c in L_a -> Bl;  else "2+1" with c in L_b \ N(a)
+            for (int64_t base = b0; base < b1; base += 32) {
+                const int64_t p = base + lane;
+                int col = kNone;
+                uint32_t c = 0;
+                if (p < b1) {
+                    const uint32_t e = g.adj[p];
+                    c = e >> 2;
+                    if (c > r) {
+                        const int pos = find_rank(R, D, c);
+                        if (pos >= 0) {
+                            if (pos > j) set2(Bb, pos, e & 3u);
+                        } else {
+                            const int q = find_rank(La, nL, c);
+                            if (q >= 0) set2(Bl, q, e & 3u);
+                            else col = lut[mb | (e & 3u) << 10];
+                        }
+                    }
+                }
+                emit4<C>(H, acc, b, c, col, lane);
+            }
+            __syncwarp();
+            // "3": c in R after b
+            for (int base = j + 1; base < D; base += 32) {
+                const int p = base + lane;
+                int col = kNone;
+                uint32_t c = 0;
+                if (p < D) {
+                    const uint32_t ec = R[p];
+                    c = ec >> 2;
+                    col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
+                }
+                emit4<C>(H, acc, b, c, col, lane);
+            }
+            // "2+1": c in L_a
+            for (int base = 0; base < nL; base += 32) {
+                const int q = base + lane;
+                int col = kNone;
+                uint32_t c = 0;
+                if (q < nL) {
+                    const uint32_t ec = La[q];
+                    c = ec >> 2;
+                    col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
+                }
+                emit4<C>(H, acc, b, c, col, lane);
+            }
+            __syncwarp();
+            clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
+            clear_words(Bl, 0, (nL + 15) >> 4, lane);
+            if (g.big) flush_hist<C>(H, acc, r, a, lane);
+            __syncwarp();
+        }
+        for (int x = w; x < nL; x += NW) {                        // b = L_a[x]
+            const uint32_t eb = La[x], b = eb >> 2;
+            const uint32_t mb = cra | (eb & 3u) << 6;
+            const int64_t b0 = g.off[b], b1 = g.off[b + 1];
+            // walk N(b): c in R -> skip;  c in L_a after b -> Bl ("1+2");  else "1+1+1"
+            for (int64_t base = b0; base < b1; base += 32) {
+                const int64_t p = base + lane;
+                int col = kNone;
+                uint32_t c = 0;
+                if (p < b1) {
+                    const uint32_t e = g.adj[p];
+                    c = e >> 2;
+                    if (c > r && find_rank(R, D, c) < 0) {
+                        const int q = find_rank(La, nL, c);
+                        if (q >= 0) {
+                            if (q > x) set2(Bl, q, e & 3u);
+                        } else {
+                            col = lut[mb | (e & 3u) << 10];
+                        }
+                    }
+                }
+                emit4<C>(H, acc, b, c, col, lane);
+            }
+            __syncwarp();
+            // "1+2": c in L_a after b
+            for (int base = x + 1; base < nL; base += 32) {
+                const int q = base + lane;
+                int col = kNone;
+                uint32_t c = 0;
+                if (q < nL) {
+                    const uint32_t ec = La[q];
+                    c = ec >> 2;
+                    col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
+                }
+                emit4<C>(H, acc, b, c, col, lane);
+            }
+            __syncwarp();
+            clear_words(Bl, (x + 1) >> 4, (nL + 15) >> 4, lane);
+            if (g.big) flush_hist<C>(H, acc, r, a, lane);
+            __syncwarp();
+        }
+    }
+}
+
 template <int K>
-__global__ void __launch_bounds__(kBlock) k_enum(Dev g, int64_t lo, int64_t hi, unsigned long long *ctr,
-                                                  const uint8_t *__restrict__ lut_g, uint32_t *__restrict__ lscr,
-                                                  int64_t lcap) {
+__global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo, int64_t hi,
+                                                     unsigned long long *ctr, const uint8_t *__restrict__ lut_g) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     constexpr int NM = K == 3 ? 64 : 4096;
+    extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
-    __shared__ unsigned long long wcnt_all[kWarps][C];
-    for (int i = threadIdx.x; i < NM; i += kBlock) lut[i] = lut_g[i];
-    for (int i = threadIdx.x; i < kWarps * C; i += kBlock) (&wcnt_all[0][0])[i] = 0;
+    __shared__ int64_t s_item;
+    __shared__ int s_nL;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
+    for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
+    uint32_t *H = sm + L.hist + wid * C;
+
+    // ---------------- heavy phase: one CTA per task (r, a)
+    {
+        uint32_t *hb = g.heavy_in_smem ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
+        uint32_t *R = hb + L.R, *La = hb + L.La, *Ba = hb + L.Ba;
+        uint32_t *Bb = hb + L.Bb + wid * L.bw, *Bl = hb + L.Bl + wid * L.lw;
+        if (!g.heavy_in_smem) {   // zero this CTA's global bitmaps once
+            for (int q = tid; q < L.Bl + kWarps * L.lw - L.Ba; q += kBlock) hb[L.Ba + q] = 0;
+        }
+        __syncthreads();
+        int64_t staged = -1;
+        for (;;) {
+            if (tid == 0) s_item = (int64_t)atomicAdd(ctr, 1ull);
+            __syncthreads();
+            const int64_t h = s_item;
+            __syncthreads();
+            if (h >= g.nheavy) break;
+            const int64_t t = g.heavy_task[h];
+            if (t < lo || t >= hi) continue;
+            const uint32_t r = (uint32_t)g.task_root[t];
+            const int64_t rs = g.split[r];
+            const int D = (int)(g.off[r + 1] - rs);
+            const int i = (int)(t - g.tfirst[r]);
+            if (staged != r) {
+                for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
+                staged = r;
+                __syncthreads();
+            }
+            if (wid == 0) {
+                const int nL = build_a(g, r, R[i] >> 2, R, D, Ba, La, lane);
+                if (lane == 0) s_nL = nL;
+            }
+            __syncthreads();
+            const int nL = s_nL;
+            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, wid, lane);
+            flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
+            __syncthreads();
+            for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
+            __syncthreads();
+        }
+    }
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long *wcnt = wcnt_all[wid];
-    uint32_t *L = lscr + (blockIdx.x * (int64_t)kWarps + wid) * lcap;
-    const uint32_t *__restrict__ adj = g.adj;
-    unsigned long long *__restrict__ acc = g.acc;
+    for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;   // light region overlays the heavy one
+    __syncthreads();
 
-    for (;;) {
-        unsigned long long t0 = 0;
-        if (lane == 0) t0 = atomicAdd(ctr, 1ull);
-        const int64_t t = lo + (int64_t)__shfl_sync(kFull, t0, 0);
-        if (t >= hi) break;
-        const uint32_t r = (uint32_t)g.task_root[t];
-        const int64_t rs = g.split[r], re = g.off[r + 1];
-        const int64_t ia = rs + (t - g.tfirst[r]);   // a's entry in r's list
-        const uint32_t ea = adj[ia];
-        const uint32_t a = ea >> 2, cra = ea & 3u;
-        const int64_t a0 = g.off[a], a1 = g.off[a + 1];
-        const int64_t as = lower_rank(adj, a0, a1, r + 1);   // a's entries with rank > r
-
-        if constexpr (K == 3) {
-            // "2": b in N+(r) after a.  mask (r,a) | (r,b) << 2 | (a,b) << 4
-            for (int64_t base = ia + 1; base < re; base += 32) {
-                const int64_t p = base + lane;
-                int col = kNoClass;
-                if (p < re) {
-                    const uint32_t eb = adj[p], b = eb >> 2;
-                    col = lut[cra | (eb & 3u) << 2 | pair_code(g, a, b) << 4];
-                    atomicAdd(acc + (size_t)b * C + col, 1ull);
-                }
-                add_root(wcnt, col, lane);
-            }
-            // "1+1": b in L_a.  (r,b) = 0
-            for (int64_t base = as; base < a1; base += 32) {
-                const int64_t p = base + lane;
-                int col = kNoClass;
-                if (p < a1) {
-                    const uint32_t eb = adj[p], b = eb >> 2;
-                    if (code_in(adj, rs, re, b) == 0) {
-                        col = lut[cra | (eb & 3u) << 4];
-                        atomicAdd(acc + (size_t)b * C + col, 1ull);
-                    }
-                }
-                add_root(wcnt, col, lane);
-            }
-        } else {
-            // L_a = N+(a) \ N(r): entries of a's list (code (a, x)) kept in the warp's scratch
-            int nL = 0;
-            for (int64_t base = as; base < a1; base += 32) {
-                const int64_t p = base + lane;
-                bool keep = false;
-                uint32_t e = 0;
-                if (p < a1) {
-                    e = adj[p];
-                    keep = code_in(adj, rs, re, e >> 2) == 0;
-                }
-                const unsigned bal = __ballot_sync(kFull, keep);
-                if (keep) L[nL + __popc(bal & ((1u << lane) - 1u))] = e;
-                nL += __popc(bal);
-            }
+    // ---------------- light phase: one warp per root, its tasks in sequence
+    {
+        uint32_t *lw = sm + L.light + wid * kLightWords;
+        uint32_t *R = lw, *Las = lw + kLW, *Ba = lw + 2 * kLW, *Bb = Ba + kLB, *Bls = Bb + kLB;
+        uint32_t *gw = g.glight + ((int64_t)blockIdx.x * kWarps + wid) * g.glight_per_warp;   // oversize L_a
+        for (;;) {
+            unsigned long long x = 0;
+            if (lane == 0) x = atomicAdd(ctr + 1, 1ull);
+            const int64_t li = (int64_t)__shfl_sync(kFull, x, 0);
+            if (li >= g.nlight) break;
+            const uint32_t r = (uint32_t)g.light_root[li];
+            const int64_t t0 = g.tfirst[r], t1 = g.tfirst[r + 1];
+            const int64_t ta = max(t0, lo), tb = min(t1, hi);
+            if (ta >= tb) continue;
+            const int64_t rs = g.split[r];
+            const int D = (int)(g.off[r + 1] - rs);
+            for (int q = lane; q < D; q += 32) R[q] = g.adj[rs + q];
             __syncwarp();
-            // mask: (r,a) | (r,b)<<2 | (r,c)<<4 | (a,b)<<6 | (a,c)<<8 | (b,c)<<10
-            for (int64_t jb = ia + 1; jb < re; jb++) {           // b in N+(r) after a
-                const uint32_t eb = adj[jb], b = eb >> 2;
-                const uint32_t mb = cra | (eb & 3u) << 2 | pair_code(g, a, b) << 6;
-                // "3": c in N+(r) after b
-                for (int64_t base = jb + 1; base < re; base += 32) {
-                    const int64_t p = base + lane;
-                    int col = kNoClass;
-                    if (p < re) {
-                        const uint32_t ec = adj[p], c = ec >> 2;
-                        col = lut[mb | (ec & 3u) << 4 | pair_code(g, a, c) << 8 | pair_code(g, b, c) << 10];
-                        atomicAdd(acc + (size_t)c * C + col, 1ull);
-                    }
-                    add_root_b<C>(wcnt, acc, b, col, lane);
+            for (int64_t t = ta; t < tb; t++) {
+                const int i = (int)(t - t0);
+                const uint32_t a = R[i] >> 2;
+                const int da = (int)(g.off[a + 1] - g.off[a]);
+                uint32_t *La = Las, *Bl = Bls;
+                if (da > kLW) {   // only with a user-given order: lists longer than the smem slots
+                    La = gw;
+                    Bl = gw + g.maxdeg;
+                    clear_words(Bl, 0, (da + 15) >> 4, lane);
+                    __syncwarp();
                 }
-                // "2+1", c in L_a:  (a,c) from a's list, (b,c) by search
-                for (int base = 0; base < nL; base += 32) {
-                    const int q = base + lane;
-                    int col = kNoClass;
-                    if (q < nL) {
-                        const uint32_t ec = L[q], c = ec >> 2;
-                        col = lut[mb | (ec & 3u) << 8 | pair_code(g, b, c) << 10];
-                        atomicAdd(acc + (size_t)c * C + col, 1ull);
-                    }
-                    add_root_b<C>(wcnt, acc, b, col, lane);
-                }
-                // "2+1", c in L_b \ N(a):  (b,c) from b's list, (a,c) = 0
-                const int64_t b1 = g.off[b + 1];
-                const int64_t bs = lower_rank(adj, g.off[b], b1, r + 1);
-                for (int64_t base = bs; base < b1; base += 32) {
-                    const int64_t p = base + lane;
-                    int col = kNoClass;
-                    if (p < b1) {
-                        const uint32_t ec = adj[p], c = ec >> 2;
-                        if (code_in(adj, rs, re, c) == 0 && pair_code(g, a, c) == 0) {
-                            col = lut[mb | (ec & 3u) << 10];
-                            atomicAdd(acc + (size_t)c * C + col, 1ull);
-                        }
-                    }
-                    add_root_b<C>(wcnt, acc, b, col, lane);
-                }
-            }
-            for (int x = 0; x < nL; x++) {                        // b in L_a
-                const uint32_t eb = L[x], b = eb >> 2;
-                const uint32_t mb = cra | (eb & 3u) << 6;
-                // "1+2": c in L_a after b
-                for (int base = x + 1; base < nL; base += 32) {
-                    const int q = base + lane;
-                    int col = kNoClass;
-                    if (q < nL) {
-                        const uint32_t ec = L[q], c = ec >> 2;
-                        col = lut[mb | (ec & 3u) << 8 | pair_code(g, b, c) << 10];
-                        atomicAdd(acc + (size_t)c * C + col, 1ull);
-                    }
-                    add_root_b<C>(wcnt, acc, b, col, lane);
-                }
-                // "1+1+1": c in N+(b) \ N(r) \ N(a)  (Lemma 4: c may have global depth 2)
-                const int64_t b1 = g.off[b + 1];
-                const int64_t bs = lower_rank(adj, g.off[b], b1, r + 1);
-                for (int64_t base = bs; base < b1; base += 32) {
-                    const int64_t p = base + lane;
-                    int col = kNoClass;
-                    if (p < b1) {
-                        const uint32_t ec = adj[p], c = ec >> 2;
-                        if (code_in(adj, rs, re, c) == 0 && pair_code(g, a, c) == 0) {
-                            col = lut[mb | (ec & 3u) << 10];
-                            atomicAdd(acc + (size_t)c * C + col, 1ull);
-                        }
-                    }
-                    add_root_b<C>(wcnt, acc, b, col, lane);
-                }
-            }
-            __syncwarp();
-        }
-        // flush the task's histogram into rows r and a
-        __syncwarp();
-        for (int j = lane; j < C; j += 32) {
-            const unsigned long long v = wcnt[j];
-            if (v) {
-                atomicAdd(acc + (size_t)r * C + j, v);
-                atomicAdd(acc + (size_t)a * C + j, v);
-                wcnt[j] = 0;
+                const int nL = build_a(g, r, a, R, D, Ba, La, lane);
+                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, 0, lane);
+                flush_hist<C>(H, g.acc, r, a, lane);
+                clear_words(Ba, 0, (D + 15) >> 4, lane);
+                __syncwarp();
             }
         }
-        __syncwarp();
     }
 }
 
@@ -280,6 +431,47 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
     }
 }
 
+// root classes: heavy = G_U degree > kLightDeg (only roots with at least one task)
+__global__ void k_root_flags(int64_t n, const int64_t *__restrict__ off, const int64_t *__restrict__ tfirst,
+                             char *__restrict__ heavy, char *__restrict__ light) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const bool has = tfirst[r + 1] > tfirst[r];
+        const bool h = off[r + 1] - off[r] > kLightDeg;
+        heavy[r] = has && h;
+        light[r] = has && !h;
+    }
+}
+
+__global__ void k_task_flags(int64_t ntasks, const int32_t *__restrict__ task_root, const char *__restrict__ heavy,
+                             char *__restrict__ flag) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntasks; t += (int64_t)gridDim.x * blockDim.x)
+        flag[t] = heavy[task_root[t]];
+}
+
+Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_words, bool force_global) {
+    Layout L{};
+    const int md = std::max(maxdeg, 1);
+    L.bw = (md + 15) / 16;
+    L.lw = (md + 15) / 16;
+    // heavy buffers (offsets relative to the heavy base)
+    L.R = 0;
+    L.La = L.R + md;
+    L.Ba = L.La + md;
+    L.Bb = L.Ba + L.bw;
+    L.Bl = L.Bb + kWarps * L.bw;
+    const int heavy_words = L.Bl + kWarps * L.lw;
+    const int light_words = kWarps * kLightWords;
+    const int hist_words = kWarps * C;
+    const int budget_words = (104 * 1024) / 4 - hist_words;   // keep 2 CTAs per SM
+    heavy_in_smem = heavy_words <= budget_words && !force_global;
+    const int region = std::max(light_words, heavy_in_smem ? heavy_words : 0);
+    L.light = 0;
+    L.hist = region;
+    L.total = region + hist_words;
+    per_cta_words = heavy_in_smem ? 0 : heavy_words;
+    return L;
+}
+
 }  // namespace
 
 vdmc_status ensure_acc(vdmc_graph *g, int k) {
@@ -301,6 +493,47 @@ vdmc_status ensure_acc(vdmc_graph *g, int k) {
         VDMC_CUDA(cudaMalloc(&g->lut4, 4096));
         VDMC_CUDA(cudaMemcpy(g->lut4, host_lut(4), 4096, cudaMemcpyHostToDevice));
     }
+    return VDMC_OK;
+}
+
+// heavy / light work lists (S4 schedule), cached in the graph
+static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
+    if (g->roots_ready) return VDMC_OK;
+    const int64_t n = g->n, T = g->ntasks;
+    char *fh = nullptr, *fl = nullptr, *ft = nullptr;
+    int64_t *nsel = nullptr;
+    VDMC_CUDA(cudaMallocAsync(&fh, std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(cudaMallocAsync(&fl, std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(cudaMallocAsync(&ft, std::max<int64_t>(T, 1), s));
+    VDMC_CUDA(cudaMallocAsync(&nsel, sizeof(int64_t) * 2, s));
+    if (!g->light_root) VDMC_CUDA(cudaMalloc(&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+    if (!g->heavy_task) VDMC_CUDA(cudaMalloc(&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1)));
+    int64_t hn[2] = {0, 0};
+    if (n > 0 && T > 0) {
+        k_root_flags<<<148 * 8, 256, 0, s>>>(n, g->off, g->tfirst, fh, fl);
+        VDMC_LAUNCH();
+        k_task_flags<<<148 * 8, 256, 0, s>>>(T, g->task_root, fh, ft);
+        VDMC_LAUNCH();
+        thrust::counting_iterator<int32_t> ids(0);
+        size_t tb = 0, tb2 = 0;
+        VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
+        VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
+        void *ts = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&ts, std::max(tb, tb2), s));
+        VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
+        VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
+        count_launch(2);
+        VDMC_CUDA(cudaMemcpyAsync(hn, nsel, sizeof hn, cudaMemcpyDeviceToHost, s));
+        cudaFreeAsync(ts, s);
+    }
+    cudaFreeAsync(fh, s);
+    cudaFreeAsync(fl, s);
+    cudaFreeAsync(ft, s);
+    cudaFreeAsync(nsel, s);
+    VDMC_CUDA(cudaStreamSynchronize(s));
+    g->nheavy = hn[0];
+    g->nlight = hn[1];
+    g->roots_ready = 1;
     return VDMC_OK;
 }
 
@@ -329,28 +562,55 @@ vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t s) {
 template <int K>
 static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, cudaStream_t s) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
-    int dev = g->device, nsm = 0, per_sm = 0;
+    const int dev = g->device;
+    int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enum<K>, kBlock, 0));
+    vdmc_status st = ensure_roots(g, s);
+    if (st) return st;
+    bool heavy_in_smem = true;
+    int64_t per_cta = 0;
+    // VDMC_HEAVY_GLOBAL=1 forces the global-memory fallback for heavy-task buffers (tests)
+    const char *force = getenv("VDMC_HEAVY_GLOBAL");
+    const Layout L = make_layout((int)g->max_degree, C, heavy_in_smem, per_cta, force && force[0] == '1');
+    const size_t smem = (size_t)L.total * 4;
+    VDMC_CUDA(cudaFuncSetAttribute(k_enum<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enum<K>, kBlock, smem));
     const int grid = std::max(1, nsm * std::max(per_sm, 1));
-    const int64_t lcap = std::max<int64_t>(g->max_degree, 1);
-    if (K == 4) {
-        const size_t need = (size_t)grid * kWarps * lcap;
-        if (g->lscratch_elems < need) {
-            if (g->lscratch) cudaFree(g->lscratch);
-            g->lscratch = nullptr;
-            g->lscratch_elems = 0;
-            VDMC_CUDA(cudaMalloc(&g->lscratch, need * sizeof(uint32_t)));
-            g->lscratch_elems = need;
-        }
+    // global fallback scratch: heavy per-CTA buffers (huge degrees), light per-warp oversize L_a
+    const int64_t per_warp = (int64_t)g->max_degree + (g->max_degree + 15) / 16 + 1;
+    const size_t need = (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
+    if (g->lscratch_elems < need) {
+        if (g->lscratch) cudaFree(g->lscratch);
+        g->lscratch = nullptr;
+        g->lscratch_elems = 0;
+        VDMC_CUDA(cudaMalloc(&g->lscratch, need * sizeof(uint32_t)));
+        g->lscratch_elems = need;
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
     VDMC_CUDA(cudaMemsetAsync(g->acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
-    VDMC_CUDA(cudaMemsetAsync(g->ctr, 0, sizeof(unsigned long long), s));
+    VDMC_CUDA(cudaMemsetAsync(g->ctr, 0, 2 * sizeof(unsigned long long), s));
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[1], s));
-    Dev d{g->off, g->split, g->adj, g->tfirst, g->task_root, (unsigned long long *)g->acc};
+    Dev d{};
+    d.off = g->off;
+    d.split = g->split;
+    d.adj = g->adj;
+    d.tfirst = g->tfirst;
+    d.task_root = g->task_root;
+    d.heavy_task = g->heavy_task;
+    d.light_root = g->light_root;
+    d.nheavy = g->nheavy;
+    d.nlight = g->nlight;
+    d.acc = (unsigned long long *)g->acc;
+    d.gheavy = g->lscratch;
+    d.glight = g->lscratch + (size_t)grid * per_cta;
+    d.gheavy_per_cta = per_cta;
+    d.glight_per_warp = per_warp;
+    d.heavy_in_smem = heavy_in_smem ? 1 : 0;
+    d.big = g->max_degree > 32767 ? 1 : 0;
+    d.maxdeg = (int)g->max_degree;
     if (hi > lo) {
-        k_enum<K><<<grid, kBlock, 0, s>>>(d, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4, g->lscratch, lcap);
+        k_enum<K><<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4);
         VDMC_LAUNCH();
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[2], s));

@@ -70,6 +70,11 @@ struct vdmc_graph {
     uint8_t *lut3 = nullptr, *lut4 = nullptr;
     int64_t *cost = nullptr;       // [ntasks] inclusive prefix of the plan's cost proxy
     int cost_k = 0;
+    // schedule: tasks of heavy roots (CTA per task) and light roots (warp per root), rank order
+    int32_t *heavy_task = nullptr; // [nheavy]
+    int32_t *light_root = nullptr; // [nlight]
+    int64_t nheavy = 0, nlight = 0;
+    int roots_ready = 0;
     // profiling
     int profiling = 0;
     cudaEvent_t ev[8] = {};

@@ -89,6 +89,21 @@ def test_rank_invariance(vd, oracle_mod, k):
 
 
 @pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("mode", ["smem", "global", "random-rank"])
+def test_heavy_and_light_paths(vd, oracle_mod, k, mode, monkeypatch):
+    """A graph with roots on both sides of the light/heavy threshold (G_U degree 256): heavy
+    tasks with buffers in shared memory, forced into the global-memory fallback, and a random
+    vertex order (light roots next to long lists: the oversize-L_a fallback)."""
+    g = G.make_config("cfg3", scale=0.03)
+    deg = np.bincount(np.concatenate([g[1], g[2]]), minlength=g[0])
+    assert deg.max() > 300
+    if mode == "global":
+        monkeypatch.setenv("VDMC_HEAVY_GLOBAL", "1")
+    rank = np.random.default_rng(3).permutation(g[0]) if mode == "random-rank" else None
+    assert np.array_equal(gpu_count(vd, g, k, rank=rank), oracle_mod.count_esu(g, k))
+
+
+@pytest.mark.parametrize("k", [3, 4])
 def test_single_motif_graphs(vd, oracle_mod, k):
     """All 54 / 3834 labelled connected motifs, one per component, randomly relabelled."""
     t = oracle_mod.class_table(k)
