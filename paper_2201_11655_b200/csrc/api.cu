@@ -330,7 +330,8 @@ void vdmc_free_graph(vdmc_graph *g) {
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
     void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->acc,
-                    g->lscratch, g->ctr, g->lut3, g->lut4, g->cost, g->heavy_task, g->light_root};
+                    g->lscratch, g->ctr, g->lut3, g->lut4, g->cost, g->heavy_task, g->light_root,
+                    g->hroots, g->hbase, g->nr_off, g->nr_adj};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (auto &e : g->ev)

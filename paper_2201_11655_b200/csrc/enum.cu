@@ -64,6 +64,9 @@ struct Dev {
     int heavy_in_smem;                        // heavy buffers fit in shared memory
     int big;                                  // degrees so large a task could overflow u32 histograms
     int maxdeg;
+    const int64_t *__restrict__ hbase;        // heavy root -> segment of nr_off
+    const int64_t *__restrict__ nr_off;       // induced adjacency of N+(r), position space
+    const uint32_t *__restrict__ nr_adj;
 };
 
 // shared-memory layout (words), computed on the host
@@ -91,6 +94,7 @@ __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x)
     return (lo < len && (S[lo] >> 2) == x) ? lo : -1;
 }
 
+__device__ __forceinline__ uint32_t swap2(uint32_t c) { return ((c & 1u) << 1) | (c >> 1); }
 __device__ __forceinline__ uint32_t get2(const uint32_t *B, int p) { return (B[p >> 4] >> ((p & 15) << 1)) & 3u; }
 __device__ __forceinline__ void set2(uint32_t *B, int p, uint32_t code) { atomicOr(B + (p >> 4), code << ((p & 15) << 1)); }
 
@@ -169,6 +173,71 @@ __device__ int build_a(const Dev &g, uint32_t r, uint32_t a, const uint32_t *R, 
     return nL;
 }
 
+// Shape "3" of a heavy task (r, a = R[i]), loops interchanged: lane = c (consecutive
+// positions of R), warp-uniform b = R[j], j in (i, pos(c)).  code(b, c) comes from the
+// root's induced adjacency in position space (pre-pass k_nr), walked by a per-lane pointer;
+// code(a, c) from Ba.  Accumulation: c in a 4-slot per-lane register cache (a run of equal
+// columns costs one atomic), b merged per iteration with __match_any_sync, r and a in H.
+template <int C, int NW>
+__device__ void star3_heavy(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
+                            const uint32_t *Ba, uint32_t cra, uint32_t a, uint32_t *H, int w, int lane) {
+    unsigned long long *__restrict__ acc = g.acc;
+    const int64_t seg = g.hbase[r];
+    for (int cb = i + 2 + w * 32; cb < D; cb += NW * 32) {
+        const int p = cb + lane;
+        const bool vc = p < D;
+        uint32_t c = 0, mc = 0, ne = 0xffffffffu;
+        int64_t q = 0, q1 = 0;
+        if (vc) {
+            const uint32_t ec = R[p];
+            c = ec >> 2;
+            mc = cra | (ec & 3u) << 4 | get2(Ba, p) << 8;
+            q = g.nr_off[seg + p];
+            q1 = g.nr_off[seg + p + 1];
+            ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
+            while ((ne >> 2) <= (uint32_t)i) {           // induced neighbours up to a: not b's
+                q++;
+                ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
+            }
+        }
+        int k0 = kNone, k1 = kNone, k2 = kNone, k3 = kNone;
+        uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+        const int pmax = min(cb + 31, D - 1);
+        for (int j = i + 1; j < pmax; j++) {
+            const uint32_t eb = R[j];
+            uint32_t cbc = 0;
+            if ((ne >> 2) == (uint32_t)j) {
+                cbc = swap2(ne & 3u);                       // entry holds code(c, b)
+                q++;
+                ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
+            }
+            const bool valid = vc && j < p;
+            const int col = valid ? (int)lut[mc | (eb & 3u) << 2 | get2(Ba, j) << 6 | cbc << 10] : kNone;
+            if (valid) {
+                if (col == k0) n0++;
+                else if (col == k1) n1++;
+                else if (col == k2) n2++;
+                else if (col == k3) n3++;
+                else {
+                    if (n3) atomicAdd(acc + (size_t)c * C + k3, (unsigned long long)n3);
+                    k3 = k2; n3 = n2; k2 = k1; n2 = n1; k1 = k0; n1 = n0; k0 = col; n0 = 1;
+                }
+            }
+            const unsigned m = __match_any_sync(kFull, col);
+            if (col != kNone && lane == __ffs(m) - 1) {
+                const unsigned cnt = __popc(m);
+                H[col] += cnt;
+                atomicAdd(acc + (size_t)(eb >> 2) * C + col, (unsigned long long)cnt);
+            }
+        }
+        if (n0) atomicAdd(acc + (size_t)c * C + k0, (unsigned long long)n0);
+        if (n1) atomicAdd(acc + (size_t)c * C + k1, (unsigned long long)n1);
+        if (n2) atomicAdd(acc + (size_t)c * C + k2, (unsigned long long)n2);
+        if (n3) atomicAdd(acc + (size_t)c * C + k3, (unsigned long long)n3);
+        if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    }
+}
+
 // The task (r, a = R[i]) for a team of NW warps (warp w of the team).  Ba/La must be built
 // (phase A) and visible to the team.  Bb/Bl are this warp's scratch bitmaps (all zero on
 // entry and exit).  H is this warp's histogram.
@@ -207,6 +276,7 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
         if (g.big) flush_hist<C>(H, acc, r, a, lane);
     } else {
         // mask: (r,a) | (r,b)<<2 | (r,c)<<4 | (a,b)<<6 | (a,c)<<8 | (b,c)<<10
+        if constexpr (NW > 1) star3_heavy<C, NW>(g, lut, r, i, R, D, Ba, cra, a, H, w, lane);
         for (int j = i + 1 + w; j < D; j += NW) {                // b = R[j]
             const uint32_t eb = R[j], b = eb >> 2;
             const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
@@ -222,7 +292,7 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
                     if (c > r) {
                         const int pos = find_rank(R, D, c);
                         if (pos >= 0) {
-                            if (pos > j) set2(Bb, pos, e & 3u);
+                            if (NW == 1 && pos > j) set2(Bb, pos, e & 3u);
                         } else {
                             const int q = find_rank(La, nL, c);
                             if (q >= 0) set2(Bl, q, e & 3u);
@@ -233,8 +303,8 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
                 emit4<C>(H, acc, b, c, col, lane);
             }
             __syncwarp();
-            // "3": c in R after b
-            for (int base = j + 1; base < D; base += 32) {
+            // "3": c in R after b (light tasks; heavy tasks ran star3_heavy)
+            for (int base = j + 1; NW == 1 && base < D; base += 32) {
                 const int p = base + lane;
                 int col = kNone;
                 uint32_t c = 0;
@@ -442,6 +512,72 @@ __global__ void k_root_flags(int64_t n, const int64_t *__restrict__ off, const i
     }
 }
 
+// S4 pre-pass for heavy roots: the induced adjacency of R = N+(r) in position space.  For
+// x = R[q], the positions p of R whose vertex is a neighbour of x, with code(x, R[p]),
+// ascending in p (x's list is sorted by rank and R is sorted by rank).  FILL = false counts,
+// FILL = true writes.  One CTA per heavy root (atomic counter), one warp per position q.
+template <bool FILL>
+__global__ void __launch_bounds__(512) k_nr(const int64_t *__restrict__ off, const int64_t *__restrict__ split,
+                                            const uint32_t *__restrict__ adj, const int32_t *__restrict__ hroots,
+                                            int64_t nh, const int64_t *__restrict__ hbase, int64_t *__restrict__ cnt,
+                                            const int64_t *__restrict__ nr_off, uint32_t *__restrict__ nr_adj,
+                                            unsigned long long *ctr, int smem_cap) {
+    extern __shared__ uint32_t Rs[];
+    __shared__ int64_t s_h;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_h = (int64_t)atomicAdd(ctr, 1ull);
+        __syncthreads();
+        const int64_t h = s_h;
+        __syncthreads();
+        if (h >= nh) break;
+        const uint32_t r = (uint32_t)hroots[h];
+        const int64_t rs = split[r];
+        const int D = (int)(off[r + 1] - rs);
+        const uint32_t *R = adj + rs;
+        if (D <= smem_cap) {
+            for (int q = threadIdx.x; q < D; q += blockDim.x) Rs[q] = adj[rs + q];
+            __syncthreads();
+            R = Rs;
+        }
+        const int64_t seg = hbase[r];
+        for (int q = wid; q < D; q += nw) {
+            const uint32_t x = R[q] >> 2;
+            const int64_t x0 = off[x], x1 = off[x + 1];
+            int64_t k = 0;
+            const int64_t o = FILL ? nr_off[seg + q] : 0;
+            for (int64_t base = x0; base < x1; base += 32) {
+                const int64_t p = base + lane;
+                int pos = -1;
+                uint32_t e = 0;
+                if (p < x1) {
+                    e = adj[p];
+                    if ((e >> 2) > r) pos = find_rank(R, D, e >> 2);
+                }
+                const unsigned bal = __ballot_sync(kFull, pos >= 0);
+                if (FILL && pos >= 0) nr_adj[o + k + __popc(bal & ((1u << lane) - 1u))] = ((uint32_t)pos << 2) | (e & 3u);
+                k += __popc(bal);
+            }
+            if (!FILL && lane == 0) cnt[seg + q] = k;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_heavy_d(int64_t nh, const int32_t *__restrict__ hroots, const int64_t *__restrict__ off,
+                          const int64_t *__restrict__ split, int64_t *__restrict__ dlist) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nh; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = hroots[q];
+        dlist[q] = off[r + 1] - split[r];
+    }
+}
+
+__global__ void k_scatter_hbase(int64_t nh, const int32_t *__restrict__ hroots, const int64_t *__restrict__ seg,
+                                int64_t *__restrict__ hbase) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nh; q += (int64_t)gridDim.x * blockDim.x)
+        hbase[hroots[q]] = seg[q];
+}
+
 __global__ void k_task_flags(int64_t ntasks, const int32_t *__restrict__ task_root, const char *__restrict__ heavy,
                              char *__restrict__ flag) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntasks; t += (int64_t)gridDim.x * blockDim.x)
@@ -526,6 +662,74 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         VDMC_CUDA(cudaMemcpyAsync(hn, nsel, sizeof hn, cudaMemcpyDeviceToHost, s));
         cudaFreeAsync(ts, s);
     }
+    // heavy roots (rank order) and the induced adjacency of each one's N+(r)
+    int64_t nhr = 0;
+    if (!g->hroots) VDMC_CUDA(cudaMalloc(&g->hroots, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+    if (!g->hbase) VDMC_CUDA(cudaMalloc(&g->hbase, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+    if (n > 0 && T > 0) {
+        thrust::counting_iterator<int32_t> ids(0);
+        size_t tb = 0;
+        VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, fh, g->hroots, nsel, (int)n, s));
+        void *ts = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&ts, tb, s));
+        VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, fh, g->hroots, nsel, (int)n, s));
+        count_launch(1);
+        VDMC_CUDA(cudaMemcpyAsync(&nhr, nsel, sizeof nhr, cudaMemcpyDeviceToHost, s));
+        VDMC_CUDA(cudaStreamSynchronize(s));
+        cudaFreeAsync(ts, s);
+    }
+    g->nhroots = nhr;
+    if (nhr > 0) {
+        int64_t *dlist = nullptr, *segs = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&dlist, sizeof(int64_t) * (nhr + 1), s));
+        VDMC_CUDA(cudaMallocAsync(&segs, sizeof(int64_t) * (nhr + 1), s));
+        VDMC_CUDA(cudaMemsetAsync(dlist + nhr, 0, sizeof(int64_t), s));
+        k_heavy_d<<<148 * 4, 256, 0, s>>>(nhr, g->hroots, g->off, g->split, dlist);
+        VDMC_LAUNCH();
+        size_t tb = 0;
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, dlist, segs, (int)(nhr + 1), s));
+        void *ts = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&ts, tb, s));
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts, tb, dlist, segs, (int)(nhr + 1), s));
+        count_launch(2);
+        k_scatter_hbase<<<148 * 4, 256, 0, s>>>(nhr, g->hroots, segs, g->hbase);
+        VDMC_LAUNCH();
+        int64_t sumD = 0;
+        VDMC_CUDA(cudaMemcpyAsync(&sumD, segs + nhr, sizeof sumD, cudaMemcpyDeviceToHost, s));
+        VDMC_CUDA(cudaStreamSynchronize(s));
+        cudaFreeAsync(ts, s);
+        // counts -> offsets -> entries
+        int64_t *cnt = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (sumD + 1), s));
+        VDMC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (sumD + 1), s));
+        if (g->nr_off) cudaFree(g->nr_off);
+        VDMC_CUDA(cudaMalloc(&g->nr_off, sizeof(int64_t) * (sumD + 1)));
+        const int cap = (int)std::min<int64_t>(g->max_degree, 12288);
+        const size_t sm = (size_t)std::max(cap, 1) * 4;
+        VDMC_CUDA(cudaFuncSetAttribute(k_nr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        VDMC_CUDA(cudaFuncSetAttribute(k_nr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        VDMC_CUDA(cudaMemsetAsync(g->ctr + 2, 0, 2 * sizeof(unsigned long long), s));
+        k_nr<false><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, cnt, nullptr,
+                                            nullptr, g->ctr + 2, cap);
+        VDMC_LAUNCH();
+        size_t tb2 = 0;
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
+        void *ts2 = nullptr;
+        VDMC_CUDA(cudaMallocAsync(&ts2, tb2, s));
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts2, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
+        count_launch(2);
+        VDMC_CUDA(cudaMemcpyAsync(&g->nr_total, g->nr_off + sumD, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        VDMC_CUDA(cudaStreamSynchronize(s));
+        if (g->nr_adj) cudaFree(g->nr_adj);
+        VDMC_CUDA(cudaMalloc(&g->nr_adj, sizeof(uint32_t) * std::max<int64_t>(g->nr_total, 1)));
+        k_nr<true><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, nullptr, g->nr_off,
+                                           g->nr_adj, g->ctr + 3, cap);
+        VDMC_LAUNCH();
+        cudaFreeAsync(ts2, s);
+        cudaFreeAsync(cnt, s);
+        cudaFreeAsync(dlist, s);
+        cudaFreeAsync(segs, s);
+    }
     cudaFreeAsync(fh, s);
     cudaFreeAsync(fl, s);
     cudaFreeAsync(ft, s);
@@ -565,6 +769,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const int dev = g->device;
     int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
     vdmc_status st = ensure_roots(g, s);
     if (st) return st;
     bool heavy_in_smem = true;
@@ -587,7 +792,6 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
         VDMC_CUDA(cudaMalloc(&g->lscratch, need * sizeof(uint32_t)));
         g->lscratch_elems = need;
     }
-    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
     VDMC_CUDA(cudaMemsetAsync(g->acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
     VDMC_CUDA(cudaMemsetAsync(g->ctr, 0, 2 * sizeof(unsigned long long), s));
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[1], s));
@@ -601,6 +805,11 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.light_root = g->light_root;
     d.nheavy = g->nheavy;
     d.nlight = g->nlight;
+    // VDMC_PHASES (profiling only; results incomplete): 1 = heavy phase only, 2 = light only
+    if (const char *ph = getenv("VDMC_PHASES")) {
+        if (ph[0] == '1') d.nlight = 0;
+        if (ph[0] == '2') d.nheavy = 0;
+    }
     d.acc = (unsigned long long *)g->acc;
     d.gheavy = g->lscratch;
     d.glight = g->lscratch + (size_t)grid * per_cta;
@@ -609,6 +818,9 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.heavy_in_smem = heavy_in_smem ? 1 : 0;
     d.big = g->max_degree > 32767 ? 1 : 0;
     d.maxdeg = (int)g->max_degree;
+    d.hbase = g->hbase;
+    d.nr_off = g->nr_off;
+    d.nr_adj = g->nr_adj;
     if (hi > lo) {
         k_enum<K><<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4);
         VDMC_LAUNCH();

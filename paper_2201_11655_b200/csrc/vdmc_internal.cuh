@@ -75,6 +75,14 @@ struct vdmc_graph {
     int32_t *light_root = nullptr; // [nlight]
     int64_t nheavy = 0, nlight = 0;
     int roots_ready = 0;
+    // induced adjacency of N+(r) in position space for heavy roots r (S4 pre-pass):
+    // entries of the position p of root r: nr_adj[nr_off[hbase[r] + p] .. nr_off[hbase[r] + p + 1])
+    int32_t *hroots = nullptr;     // [nhroots] heavy roots, rank order
+    int64_t nhroots = 0;
+    int64_t *hbase = nullptr;      // [n] segment base per heavy root
+    int64_t *nr_off = nullptr;     // [sum D+ over heavy roots + 1]
+    uint32_t *nr_adj = nullptr;    // position << 2 | code(x, R[position])
+    int64_t nr_total = 0;
     // profiling
     int profiling = 0;
     cudaEvent_t ev[8] = {};
