@@ -64,6 +64,7 @@ struct Dev {
     int heavy_in_smem;                        // heavy buffers fit in shared memory
     int big;                                  // degrees so large a task could overflow u32 histograms
     int maxdeg;
+    int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop
     const int64_t *__restrict__ hbase;        // heavy root -> segment of nr_off
     const int64_t *__restrict__ nr_off;       // induced adjacency of N+(r), position space
     const uint32_t *__restrict__ nr_adj;
@@ -174,67 +175,134 @@ __device__ int build_a(const Dev &g, uint32_t r, uint32_t a, const uint32_t *R, 
 }
 
 // Shape "3" of a heavy task (r, a = R[i]), loops interchanged: lane = c (consecutive
-// positions of R), warp-uniform b = R[j], j in (i, pos(c)).  code(b, c) comes from the
-// root's induced adjacency in position space (pre-pass k_nr), walked by a per-lane pointer;
-// code(a, c) from Ba.  Accumulation: c in a 4-slot per-lane register cache (a run of equal
-// columns costs one atomic), b merged per iteration with __match_any_sync, r and a in H.
+// positions of R), warp-uniform b = R[j], j in (i, pos(c)).  Per iteration the warp reads
+// one byte, codes[j] = code(r,b) | code(a,b) << 2; code(b, c) comes from the root's induced
+// adjacency in position space (pre-pass k_nr) through a per-lane pointer, code(a, c) from Ba.
+// A set is "plain" when code(a,b) = code(b,c) = 0 (almost all sets at a hub): then its mask,
+// hence its class, is fixed by the lane's (code(r,c), code(a,c)) and the iteration's
+// code(r,b) alone, so
+//   * c (lane) counts plain sets in three 21-bit fields of one register, indexed by
+//     code(r,b); the classes are looked up once per lane at the end of the chunk, where r
+//     and a (histogram H) and c (one atomic per non-zero field) are credited;
+//   * b (warp-uniform) gets, per lane key k = (code(r,c), code(a,c)), popc(plain & M_k)
+//     sets of class lut[key k, code(r,b)]: lanes 0..11 each own one key and issue at most
+//     one atomic;
+//   * the rare non-plain sets are classified individually (slow path).
+// Every set is still visited once and classified through the LUT (plain sets through the
+// LUT entry of their exact mask).
+// per-lane state of one c in star3_heavy
+struct StarC {
+    uint32_t c, lmask, ne;   // vertex, mask bits fixed by c, next induced neighbour (pos << 2 | code(c, x))
+    int64_t q, q1;           // walk over c's induced adjacency
+    unsigned long long packed;
+    int key;
+};
+
+__device__ __forceinline__ void star_c_init(const Dev &g, StarC &s, const uint32_t *R, int D, const uint32_t *Ba,
+                                            uint32_t cra, int i, int p, int64_t seg) {
+    s.c = 0; s.lmask = 0; s.ne = 0xffffffffu; s.q = 0; s.q1 = 0; s.packed = 0; s.key = 15;
+    if (p < D) {
+        const uint32_t ec = R[p];
+        const uint32_t crc = ec & 3u, cac = get2(Ba, p);
+        s.c = ec >> 2;
+        s.lmask = cra | crc << 4 | cac << 8;
+        s.key = (int)(crc - 1u + 3u * cac);
+        s.q = g.nr_off[seg + p];
+        s.q1 = g.nr_off[seg + p + 1];
+        for (;;) {                                       // first induced neighbour after a
+            s.ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
+            if ((s.ne >> 2) > (uint32_t)i) break;
+            s.q++;
+        }
+    }
+}
+
+// one (b = R[j], c) step for one of the lane's c; returns this lane's plain bit
+template <int C>
+__device__ __forceinline__ bool star_c_step(const Dev &g, StarC &s, const uint8_t *lut, uint32_t *H, int j,
+                                            uint32_t ub, unsigned long long inc, bool valid, uint32_t b) {
+    const bool hit = (s.ne >> 2) == (uint32_t)j;
+    const bool plain = valid && !hit && (ub >> 2) == 0;
+    if (plain) s.packed += inc;
+    if (valid && !plain) {                              // rare: a-b or b-c edge
+        const uint32_t cbc = hit ? swap2(s.ne & 3u) : 0u;   // entry holds code(c, b)
+        const int col = lut[s.lmask | (ub & 3u) << 2 | (ub >> 2) << 6 | cbc << 10];
+        atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
+        atomicAdd(g.acc + (size_t)b * C + col, 1ull);
+        atomicAdd(H + col, 1u);
+    }
+    if (hit) {
+        s.q++;
+        s.ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
+    }
+    return plain;
+}
+
+template <int C>
+__device__ __forceinline__ void star_c_flush(const Dev &g, const StarC &s, const uint8_t *lut, uint32_t *H) {
+    if (s.key == 15) return;
+#pragma unroll
+    for (uint32_t crb = 1; crb <= 3; crb++) {
+        const uint32_t nset = (uint32_t)(s.packed >> (21u * (crb - 1u))) & 0x1fffffu;
+        if (nset) {
+            const int col = lut[s.lmask | crb << 2];
+            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)nset);
+            atomicAdd(H + col, nset);
+        }
+    }
+}
+
+// Shape "3" of a heavy task (r, a = R[i]), loops interchanged: each lane owns two c's
+// (positions cb + lane and cb + 32 + lane of R), the warp walks b = R[j], j in (i, pos(c)),
+// uniformly.  Per iteration the warp reads one byte, codes[j] = code(r,b) | code(a,b) << 2;
+// code(b, c) comes from the root's induced adjacency in position space (pre-pass k_nr)
+// through a per-c pointer, code(a, c) from Ba.  A set is "plain" when code(a,b) = code(b,c)
+// = 0 (almost every set at a hub): its mask, hence its class, is then fixed by c's
+// (code(r,c), code(a,c)) and the iteration's code(r,b), so
+//   * c counts plain sets in three 21-bit fields of one register, indexed by code(r,b); the
+//     classes are looked up once per c at the end of the chunk, where r and a (histogram H)
+//     and c (one atomic per non-zero field) are credited;
+//   * b gets, per c key k = (code(r,c), code(a,c)), popc(plain & M_k) sets of class
+//     lut[key k, code(r,b)]: lanes 0..11 each own one key and issue at most one atomic;
+//   * the rare non-plain sets are classified one by one (star_c_step).
+// Every set is visited once and classified through the LUT entry of its exact mask.
 template <int C, int NW>
 __device__ void star3_heavy(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
-                            const uint32_t *Ba, uint32_t cra, uint32_t a, uint32_t *H, int w, int lane) {
+                            const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a, uint32_t *H, int w,
+                            int lane) {
     unsigned long long *__restrict__ acc = g.acc;
     const int64_t seg = g.hbase[r];
-    for (int cb = i + 2 + w * 32; cb < D; cb += NW * 32) {
-        const int p = cb + lane;
-        const bool vc = p < D;
-        uint32_t c = 0, mc = 0, ne = 0xffffffffu;
-        int64_t q = 0, q1 = 0;
-        if (vc) {
-            const uint32_t ec = R[p];
-            c = ec >> 2;
-            mc = cra | (ec & 3u) << 4 | get2(Ba, p) << 8;
-            q = g.nr_off[seg + p];
-            q1 = g.nr_off[seg + p + 1];
-            ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
-            while ((ne >> 2) <= (uint32_t)i) {           // induced neighbours up to a: not b's
-                q++;
-                ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
-            }
+    const uint32_t kcrc = (uint32_t)(lane % 3) + 1u, kcac = (uint32_t)(lane / 3);   // lanes 0..11 own a key
+    const uint32_t kmask = cra | kcrc << 4 | kcac << 8;
+    for (int cb = i + 2 + w * 64; cb < D; cb += NW * 64) {
+        StarC s0, s1;
+        star_c_init(g, s0, R, D, Ba, cra, i, cb + lane, seg);
+        star_c_init(g, s1, R, D, Ba, cra, i, cb + 32 + lane, seg);
+        unsigned M0 = 0, M1 = 0;
+#pragma unroll
+        for (int k = 0; k < 12; k++) {
+            const unsigned m0 = __ballot_sync(kFull, s0.key == k);
+            const unsigned m1 = __ballot_sync(kFull, s1.key == k);
+            if (lane == k) { M0 = m0; M1 = m1; }
         }
-        int k0 = kNone, k1 = kNone, k2 = kNone, k3 = kNone;
-        uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0;
-        const int pmax = min(cb + 31, D - 1);
+        const int pmax = min(cb + 63, D - 1);   // last c of the chunk: b runs over (i, pmax)
         for (int j = i + 1; j < pmax; j++) {
-            const uint32_t eb = R[j];
-            uint32_t cbc = 0;
-            if ((ne >> 2) == (uint32_t)j) {
-                cbc = swap2(ne & 3u);                       // entry holds code(c, b)
-                q++;
-                ne = q < q1 ? g.nr_adj[q] : 0xffffffffu;
-            }
-            const bool valid = vc && j < p;
-            const int col = valid ? (int)lut[mc | (eb & 3u) << 2 | get2(Ba, j) << 6 | cbc << 10] : kNone;
-            if (valid) {
-                if (col == k0) n0++;
-                else if (col == k1) n1++;
-                else if (col == k2) n2++;
-                else if (col == k3) n3++;
-                else {
-                    if (n3) atomicAdd(acc + (size_t)c * C + k3, (unsigned long long)n3);
-                    k3 = k2; n3 = n2; k2 = k1; n2 = n1; k1 = k0; n1 = n0; k0 = col; n0 = 1;
-                }
-            }
-            const unsigned m = __match_any_sync(kFull, col);
-            if (col != kNone && lane == __ffs(m) - 1) {
-                const unsigned cnt = __popc(m);
-                H[col] += cnt;
-                atomicAdd(acc + (size_t)(eb >> 2) * C + col, (unsigned long long)cnt);
+            const uint32_t ub = codes[j];
+            const uint32_t b = R[j] >> 2;
+            const unsigned long long inc = 1ull << (21u * ((ub & 3u) - 1u));
+            const bool v0 = cb + lane > j && cb + lane < D;
+            const bool v1 = cb + 32 + lane > j && cb + 32 + lane < D;
+            const unsigned p0 = __ballot_sync(kFull, star_c_step<C>(g, s0, lut, H, j, ub, inc, v0, b));
+            const unsigned p1 = __ballot_sync(kFull, star_c_step<C>(g, s1, lut, H, j, ub, inc, v1, b));
+            if (lane < 12) {
+                const unsigned cnt = __popc(p0 & M0) + __popc(p1 & M1);
+                if (cnt) atomicAdd(acc + (size_t)b * C + lut[kmask | (ub & 3u) << 2], (unsigned long long)cnt);
             }
         }
-        if (n0) atomicAdd(acc + (size_t)c * C + k0, (unsigned long long)n0);
-        if (n1) atomicAdd(acc + (size_t)c * C + k1, (unsigned long long)n1);
-        if (n2) atomicAdd(acc + (size_t)c * C + k2, (unsigned long long)n2);
-        if (n3) atomicAdd(acc + (size_t)c * C + k3, (unsigned long long)n3);
+        star_c_flush<C>(g, s0, lut, H);
+        star_c_flush<C>(g, s1, lut, H);
         if (g.big) flush_hist<C>(H, acc, r, a, lane);
+        __syncwarp();
     }
 }
 
@@ -244,6 +312,7 @@ __device__ void star3_heavy(const Dev &g, const uint8_t *lut, uint32_t r, int i,
 template <int K, int NW>
 __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
                            const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb, uint32_t *Bl, uint32_t *H,
+                           const uint8_t *codes,
                            int w, int lane) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
@@ -276,8 +345,9 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
         if (g.big) flush_hist<C>(H, acc, r, a, lane);
     } else {
         // mask: (r,a) | (r,b)<<2 | (r,c)<<4 | (a,b)<<6 | (a,c)<<8 | (b,c)<<10
-        if constexpr (NW > 1) star3_heavy<C, NW>(g, lut, r, i, R, D, Ba, cra, a, H, w, lane);
-        for (int j = i + 1 + w; j < D; j += NW) {                // b = R[j]
+        if constexpr (NW > 1)
+            if (!(g.skip & 1)) star3_heavy<C, NW>(g, lut, r, i, R, D, Ba, codes, cra, a, H, w, lane);
+        for (int j = i + 1 + w; !(g.skip & 2) && j < D; j += NW) {                // b = R[j]
             const uint32_t eb = R[j], b = eb >> 2;
             const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
             const int64_t b0 = g.off[b], b1 = g.off[b + 1];
@@ -328,12 +398,12 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
                 emit4<C>(H, acc, b, c, col, lane);
             }
             __syncwarp();
-            clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
+            if (NW == 1) clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
             clear_words(Bl, 0, (nL + 15) >> 4, lane);
             if (g.big) flush_hist<C>(H, acc, r, a, lane);
             __syncwarp();
         }
-        for (int x = w; x < nL; x += NW) {                        // b = L_a[x]
+        for (int x = w; !(g.skip & 4) && x < nL; x += NW) {       // b = L_a[x]
             const uint32_t eb = La[x], b = eb >> 2;
             const uint32_t mb = cra | (eb & 3u) << 6;
             const int64_t b0 = g.off[b], b1 = g.off[b + 1];
@@ -395,7 +465,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     {
         uint32_t *hb = g.heavy_in_smem ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
         uint32_t *R = hb + L.R, *La = hb + L.La, *Ba = hb + L.Ba;
-        uint32_t *Bb = hb + L.Bb + wid * L.bw, *Bl = hb + L.Bl + wid * L.lw;
+        uint32_t *Bl = hb + L.Bl + wid * L.lw;
+        uint8_t *codes = reinterpret_cast<uint8_t *>(hb + L.Bb);   // heavy: per-task code bytes
         if (!g.heavy_in_smem) {   // zero this CTA's global bitmaps once
             for (int q = tid; q < L.Bl + kWarps * L.lw - L.Ba; q += kBlock) hb[L.Ba + q] = 0;
         }
@@ -424,7 +495,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             }
             __syncthreads();
             const int nL = s_nL;
-            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, wid, lane);
+            if (K == 4) {   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2
+                for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
+                __syncthreads();
+            }
+            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -465,7 +540,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     __syncwarp();
                 }
                 const int nL = build_a(g, r, a, R, D, Ba, La, lane);
-                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, 0, lane);
+                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
@@ -593,8 +668,8 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
     L.R = 0;
     L.La = L.R + md;
     L.Ba = L.La + md;
-    L.Bb = L.Ba + L.bw;
-    L.Bl = L.Bb + kWarps * L.bw;
+    L.Bb = L.Ba + L.bw;                  // heavy: the per-task code bytes (md bytes)
+    L.Bl = L.Bb + (md + 3) / 4;
     const int heavy_words = L.Bl + kWarps * L.lw;
     const int light_words = kWarps * kLightWords;
     const int hist_words = kWarps * C;
@@ -769,6 +844,8 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const int dev = g->device;
     int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (g->max_degree >= (int64_t(1) << 21))   // star3_heavy packs per-lane counts in 21-bit fields
+        return fail(VDMC_EINVAL, "max degree %lld >= 2^21 is not supported", (long long)g->max_degree);
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
     vdmc_status st = ensure_roots(g, s);
     if (st) return st;
@@ -809,6 +886,9 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     if (const char *ph = getenv("VDMC_PHASES")) {
         if (ph[0] == '1') d.nlight = 0;
         if (ph[0] == '2') d.nheavy = 0;
+    }
+    if (const char *sk = getenv("VDMC_SKIP")) {   // profiling only; results incomplete
+        d.skip = atoi(sk);
     }
     d.acc = (unsigned long long *)g->acc;
     d.gheavy = g->lscratch;
