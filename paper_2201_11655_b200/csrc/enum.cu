@@ -174,146 +174,264 @@ __device__ int build_a(const Dev &g, uint32_t r, uint32_t a, const uint32_t *R, 
     return nL;
 }
 
-// Shape "3" of a heavy task (r, a = R[i]), loops interchanged: lane = c (consecutive
-// positions of R), warp-uniform b = R[j], j in (i, pos(c)).  Per iteration the warp reads
-// one byte, codes[j] = code(r,b) | code(a,b) << 2; code(b, c) comes from the root's induced
-// adjacency in position space (pre-pass k_nr) through a per-lane pointer, code(a, c) from Ba.
-// A set is "plain" when code(a,b) = code(b,c) = 0 (almost all sets at a hub): then its mask,
-// hence its class, is fixed by the lane's (code(r,c), code(a,c)) and the iteration's
-// code(r,b) alone, so
-//   * c (lane) counts plain sets in three 21-bit fields of one register, indexed by
-//     code(r,b); the classes are looked up once per lane at the end of the chunk, where r
-//     and a (histogram H) and c (one atomic per non-zero field) are credited;
-//   * b (warp-uniform) gets, per lane key k = (code(r,c), code(a,c)), popc(plain & M_k)
-//     sets of class lut[key k, code(r,b)]: lanes 0..11 each own one key and issue at most
-//     one atomic;
-//   * the rare non-plain sets are classified individually (slow path).
-// Every set is still visited once and classified through the LUT (plain sets through the
-// LUT entry of their exact mask).
-// per-lane state of one c in star3_heavy
+// ------------------------------------------------------------------ shape "3" at heavy roots
+// Loops interchanged: each lane owns two c's of a 64-position chunk of R, the warp walks
+// b = R[j], j in (i, pos(c)), uniformly.  Per iteration the warp reads codes[j] = code(r,b) |
+// code(a,b) << 2 (one byte) and R[j]; code(b, c) comes from the root's induced adjacency in
+// position space (pre-pass k_nr) through a per-c pointer; code(a, c) from Ba.  A set is
+// "plain" when code(a,b) = code(b,c) = 0 (almost every set at a hub); its mask, hence its
+// class, is then fixed by c's (code(r,c), code(a,c)) and the iteration's code(r,b), so
+//   * c counts its plain sets in 16-bit fields indexed by code(r,b); the classes are looked up
+//     once per c at the end of a block, where r and a (histogram H) and c are credited;
+//   * b gets, per key k = (code(r,c), code(a,c)) of c, popc(plain & M_k) sets of class
+//     lut[key k | code(r,b)]: lanes 0..11 own one key each, at most one atomic per lane;
+//   * the rare non-plain sets are classified one by one (star_slow).
+// Every set is visited once and classified through the LUT entry of its exact mask.
 struct StarC {
-    uint32_t c, lmask, ne;   // vertex, mask bits fixed by c, next induced neighbour (pos << 2 | code(c, x))
-    int64_t q, q1;           // walk over c's induced adjacency
-    unsigned long long packed;
-    int key;
+    uint32_t c, lmask, npos, ncode;   // vertex, mask bits fixed by c, next induced neighbour of c
+    int64_t q, q1;                    // walk over c's induced adjacency
+    uint32_t pA, pB;                  // plain sets: pA = n(code(r,b)=1) | n(=2) << 16, pB = n(=3)
+    int key;                          // code(r,c) - 1 + 3 code(a,c); 15 = no c
 };
+
+__device__ __forceinline__ void star_c_advance(const Dev &g, StarC &s) {
+    s.q++;
+    const uint32_t ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
+    s.npos = ne >> 2;
+    s.ncode = ne & 3u;
+}
 
 __device__ __forceinline__ void star_c_init(const Dev &g, StarC &s, const uint32_t *R, int D, const uint32_t *Ba,
                                             uint32_t cra, int i, int p, int64_t seg) {
-    s.c = 0; s.lmask = 0; s.ne = 0xffffffffu; s.q = 0; s.q1 = 0; s.packed = 0; s.key = 15;
-    if (p < D) {
+    s.c = 0; s.lmask = 0; s.npos = 0x3fffffffu; s.ncode = 0; s.q = 0; s.q1 = 0; s.pA = 0; s.pB = 0; s.key = 15;
+    if (p < D && p >= i + 2) {
         const uint32_t ec = R[p];
         const uint32_t crc = ec & 3u, cac = get2(Ba, p);
         s.c = ec >> 2;
         s.lmask = cra | crc << 4 | cac << 8;
         s.key = (int)(crc - 1u + 3u * cac);
-        s.q = g.nr_off[seg + p];
+        s.q = g.nr_off[seg + p] - 1;
         s.q1 = g.nr_off[seg + p + 1];
-        for (;;) {                                       // first induced neighbour after a
-            s.ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
-            if ((s.ne >> 2) > (uint32_t)i) break;
-            s.q++;
-        }
+        do star_c_advance(g, s);                        // first induced neighbour after a
+        while (s.npos <= (uint32_t)i);
     }
 }
 
-// one (b = R[j], c) step for one of the lane's c; returns this lane's plain bit
 template <int C>
-__device__ __forceinline__ bool star_c_step(const Dev &g, StarC &s, const uint8_t *lut, uint32_t *H, int j,
-                                            uint32_t ub, unsigned long long inc, bool valid, uint32_t b) {
-    const bool hit = (s.ne >> 2) == (uint32_t)j;
-    const bool plain = valid && !hit && (ub >> 2) == 0;
-    if (plain) s.packed += inc;
-    if (valid && !plain) {                              // rare: a-b or b-c edge
-        const uint32_t cbc = hit ? swap2(s.ne & 3u) : 0u;   // entry holds code(c, b)
-        const int col = lut[s.lmask | (ub & 3u) << 2 | (ub >> 2) << 6 | cbc << 10];
-        atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
-        atomicAdd(g.acc + (size_t)b * C + col, 1ull);
-        atomicAdd(H + col, 1u);
-    }
-    if (hit) {
-        s.q++;
-        s.ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
-    }
-    return plain;
-}
-
-template <int C>
-__device__ __forceinline__ void star_c_flush(const Dev &g, const StarC &s, const uint8_t *lut, uint32_t *H) {
+__device__ __forceinline__ void star_c_flush(const Dev &g, StarC &s, const uint8_t *lut, uint32_t *H) {
     if (s.key == 15) return;
+    const uint32_t n[3] = {s.pA & 0xffffu, s.pA >> 16, s.pB};
 #pragma unroll
     for (uint32_t crb = 1; crb <= 3; crb++) {
-        const uint32_t nset = (uint32_t)(s.packed >> (21u * (crb - 1u))) & 0x1fffffu;
-        if (nset) {
+        if (n[crb - 1]) {
             const int col = lut[s.lmask | crb << 2];
-            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)nset);
-            atomicAdd(H + col, nset);
+            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n[crb - 1]);
+            atomicAdd(H + col, n[crb - 1]);
+        }
+    }
+    s.pA = 0;
+    s.pB = 0;
+}
+
+// a set with an a-b or b-c edge: classify it alone
+template <int C>
+__device__ __forceinline__ void star_slow(const Dev &g, const StarC &s, const uint8_t *lut, uint32_t *H, uint32_t ub,
+                                          uint32_t b, bool hit) {
+    const uint32_t cbc = hit ? swap2(s.ncode) : 0u;   // the entry holds code(c, b)
+    const int col = lut[s.lmask | (ub & 3u) << 2 | (ub >> 2) << 6 | cbc << 10];
+    atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
+    atomicAdd(g.acc + (size_t)b * C + col, 1ull);
+    atomicAdd(H + col, 1u);
+}
+
+// b = R[j] for j in [j0, j1).  TAIL: some lanes' c are not after b (the chunk's own b's)
+template <int C, bool TAIL>
+__device__ __forceinline__ void star_run(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
+                                         const uint8_t *codes, StarC &s0, StarC &s1, int p0, int p1, unsigned M0,
+                                         unsigned M1, uint32_t kmask, int j0, int j1) {
+    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    for (int j = j0; j < j1; j++) {
+        const uint32_t ub = codes[j];
+        const uint32_t crb = ub & 3u;
+        const bool cabz = ub < 4u;
+        const uint32_t incA = crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u);
+        const uint32_t incB = crb == 3u ? 1u : 0u;
+        const bool h0 = s0.npos == (uint32_t)j, h1 = s1.npos == (uint32_t)j;
+        const bool v0 = TAIL ? (vc0 && p0 > j) : vc0;
+        const bool v1 = TAIL ? (vc1 && p1 > j) : vc1;
+        const bool pl0 = v0 && !h0 && cabz, pl1 = v1 && !h1 && cabz;
+        s0.pA += pl0 ? incA : 0u;
+        s0.pB += pl0 ? incB : 0u;
+        s1.pA += pl1 ? incA : 0u;
+        s1.pB += pl1 ? incB : 0u;
+        const unsigned bm0 = __ballot_sync(kFull, pl0), bm1 = __ballot_sync(kFull, pl1);
+        const uint32_t b = R[j] >> 2;
+        const unsigned cnt = __popc(bm0 & M0) + __popc(bm1 & M1);   // lanes >= 12 have M = 0
+        if (cnt) atomicAdd(g.acc + (size_t)b * C + lut[kmask | crb << 2], (unsigned long long)cnt);
+        const bool sl0 = v0 && !pl0, sl1 = v1 && !pl1;
+        if (__any_sync(kFull, sl0 || sl1 || h0 || h1)) {          // rare, warp-uniform
+            if (sl0) star_slow<C>(g, s0, lut, H, ub, b, h0);
+            if (sl1) star_slow<C>(g, s1, lut, H, ub, b, h1);
+            if (h0) star_c_advance(g, s0);
+            if (h1) star_c_advance(g, s1);
         }
     }
 }
 
-// Shape "3" of a heavy task (r, a = R[i]), loops interchanged: each lane owns two c's
-// (positions cb + lane and cb + 32 + lane of R), the warp walks b = R[j], j in (i, pos(c)),
-// uniformly.  Per iteration the warp reads one byte, codes[j] = code(r,b) | code(a,b) << 2;
-// code(b, c) comes from the root's induced adjacency in position space (pre-pass k_nr)
-// through a per-c pointer, code(a, c) from Ba.  A set is "plain" when code(a,b) = code(b,c)
-// = 0 (almost every set at a hub): its mask, hence its class, is then fixed by c's
-// (code(r,c), code(a,c)) and the iteration's code(r,b), so
-//   * c counts plain sets in three 21-bit fields of one register, indexed by code(r,b); the
-//     classes are looked up once per c at the end of the chunk, where r and a (histogram H)
-//     and c (one atomic per non-zero field) are credited;
-//   * b gets, per c key k = (code(r,c), code(a,c)), popc(plain & M_k) sets of class
-//     lut[key k, code(r,b)]: lanes 0..11 each own one key and issue at most one atomic;
-//   * the rare non-plain sets are classified one by one (star_c_step).
-// Every set is visited once and classified through the LUT entry of its exact mask.
-template <int C, int NW>
-__device__ void star3_heavy(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
-                            const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a, uint32_t *H, int w,
-                            int lane) {
-    unsigned long long *__restrict__ acc = g.acc;
+// chunk k of the task (r, a = R[i]): c positions [max(D - 64(k+1), i+2), D - 64k), the
+// longest chunks first
+template <int C>
+__device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
+                                           int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
+                                           uint32_t *H, int k, int lane) {
     const int64_t seg = g.hbase[r];
-    const uint32_t kcrc = (uint32_t)(lane % 3) + 1u, kcac = (uint32_t)(lane / 3);   // lanes 0..11 own a key
-    const uint32_t kmask = cra | kcrc << 4 | kcac << 8;
-    for (int cb = i + 2 + w * 64; cb < D; cb += NW * 64) {
-        StarC s0, s1;
-        star_c_init(g, s0, R, D, Ba, cra, i, cb + lane, seg);
-        star_c_init(g, s1, R, D, Ba, cra, i, cb + 32 + lane, seg);
-        unsigned M0 = 0, M1 = 0;
+    const int cb = D - 64 * (k + 1);
+    const int p0 = cb + lane, p1 = cb + 32 + lane;
+    StarC s0, s1;
+    star_c_init(g, s0, R, D, Ba, cra, i, p0, seg);
+    star_c_init(g, s1, R, D, Ba, cra, i, p1, seg);
+    unsigned M0 = 0, M1 = 0;
 #pragma unroll
-        for (int k = 0; k < 12; k++) {
-            const unsigned m0 = __ballot_sync(kFull, s0.key == k);
-            const unsigned m1 = __ballot_sync(kFull, s1.key == k);
-            if (lane == k) { M0 = m0; M1 = m1; }
-        }
-        const int pmax = min(cb + 63, D - 1);   // last c of the chunk: b runs over (i, pmax)
-        for (int j = i + 1; j < pmax; j++) {
-            const uint32_t ub = codes[j];
-            const uint32_t b = R[j] >> 2;
-            const unsigned long long inc = 1ull << (21u * ((ub & 3u) - 1u));
-            const bool v0 = cb + lane > j && cb + lane < D;
-            const bool v1 = cb + 32 + lane > j && cb + 32 + lane < D;
-            const unsigned p0 = __ballot_sync(kFull, star_c_step<C>(g, s0, lut, H, j, ub, inc, v0, b));
-            const unsigned p1 = __ballot_sync(kFull, star_c_step<C>(g, s1, lut, H, j, ub, inc, v1, b));
-            if (lane < 12) {
-                const unsigned cnt = __popc(p0 & M0) + __popc(p1 & M1);
-                if (cnt) atomicAdd(acc + (size_t)b * C + lut[kmask | (ub & 3u) << 2], (unsigned long long)cnt);
-            }
-        }
+    for (int q = 0; q < 12; q++) {
+        const unsigned m0 = __ballot_sync(kFull, s0.key == q), m1 = __ballot_sync(kFull, s1.key == q);
+        if (lane == q) { M0 = m0; M1 = m1; }
+    }
+    const uint32_t kmask = cra | ((uint32_t)(lane % 3) + 1u) << 4 | ((uint32_t)(lane / 3) & 3u) << 8;
+    const int jmain = max(i + 1, min(cb, D));           // b before every c of the chunk
+    const int pmax = D - 64 * k - 1;                     // last c position of the chunk
+    // 16-bit fields: flush at least every 65535 iterations
+    for (int jb = i + 1; jb < jmain; jb += 65535) {
+        star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jb, min(jmain, jb + 65535));
         star_c_flush<C>(g, s0, lut, H);
         star_c_flush<C>(g, s1, lut, H);
-        if (g.big) flush_hist<C>(H, acc, r, a, lane);
-        __syncwarp();
     }
+    star_run<C, true>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jmain, pmax);
+    star_c_flush<C>(g, s0, lut, H);
+    star_c_flush<C>(g, s1, lut, H);
+    if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
+    __syncwarp();
 }
 
-// The task (r, a = R[i]) for a team of NW warps (warp w of the team).  Ba/La must be built
-// (phase A) and visible to the team.  Bb/Bl are this warp's scratch bitmaps (all zero on
-// entry and exit).  H is this warp's histogram.
+// b = R[j] (k = 4): walk N(b) once -- c in R after b -> Bb (light tasks only; heavy tasks run
+// star_chunk), c in L_a -> Bl, else a "2+1" set with c in L_b \ N(a); then "3" over R (light)
+// and "2+1" over L_a.
+template <int C, int NW>
+__device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, uint32_t r, int i, int j,
+                                            const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La, int nL,
+                                            uint32_t *Bb, uint32_t *Bl, uint32_t *H, uint32_t cra, uint32_t a,
+                                            int lane) {
+    unsigned long long *__restrict__ acc = g.acc;
+    const uint32_t eb = R[j], b = eb >> 2;
+    const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
+    const int64_t b0 = g.off[b], b1 = g.off[b + 1];
+    for (int64_t base = b0; base < b1; base += 32) {
+        const int64_t p = base + lane;
+        int col = kNone;
+        uint32_t c = 0;
+        if (p < b1) {
+            const uint32_t e = g.adj[p];
+            c = e >> 2;
+            if (c > r) {
+                const int pos = find_rank(R, D, c);
+                if (pos >= 0) {
+                    if (NW == 1 && pos > j) set2(Bb, pos, e & 3u);
+                } else {
+                    const int q = find_rank(La, nL, c);
+                    if (q >= 0) set2(Bl, q, e & 3u);
+                    else col = lut[mb | (e & 3u) << 10];
+                }
+            }
+        }
+        emit4<C>(H, acc, b, c, col, lane);
+    }
+    __syncwarp();
+    if constexpr (NW == 1) {   // "3": c in R after b
+        for (int base = j + 1; base < D; base += 32) {
+            const int p = base + lane;
+            int col = kNone;
+            uint32_t c = 0;
+            if (p < D) {
+                const uint32_t ec = R[p];
+                c = ec >> 2;
+                col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
+            }
+            emit4<C>(H, acc, b, c, col, lane);
+        }
+    }
+    // "2+1": c in L_a
+    for (int base = 0; base < nL; base += 32) {
+        const int q = base + lane;
+        int col = kNone;
+        uint32_t c = 0;
+        if (q < nL) {
+            const uint32_t ec = La[q];
+            c = ec >> 2;
+            col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
+        }
+        emit4<C>(H, acc, b, c, col, lane);
+    }
+    __syncwarp();
+    if (NW == 1) clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
+    clear_words(Bl, 0, (nL + 15) >> 4, lane);
+    if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    __syncwarp();
+}
+
+// b = L_a[x] (k = 4): walk N(b) once -- c in R -> skip, c in L_a after b -> Bl ("1+2"), else a
+// "1+1+1" set; then "1+2" over L_a after b.
+template <int C>
+__device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, uint32_t r, int x, const uint32_t *R,
+                                             int D, const uint32_t *La, int nL, uint32_t *Bl, uint32_t *H,
+                                             uint32_t cra, uint32_t a, int lane) {
+    unsigned long long *__restrict__ acc = g.acc;
+    const uint32_t eb = La[x], b = eb >> 2;
+    const uint32_t mb = cra | (eb & 3u) << 6;
+    const int64_t b0 = g.off[b], b1 = g.off[b + 1];
+    for (int64_t base = b0; base < b1; base += 32) {
+        const int64_t p = base + lane;
+        int col = kNone;
+        uint32_t c = 0;
+        if (p < b1) {
+            const uint32_t e = g.adj[p];
+            c = e >> 2;
+            if (c > r && find_rank(R, D, c) < 0) {
+                const int q = find_rank(La, nL, c);
+                if (q >= 0) {
+                    if (q > x) set2(Bl, q, e & 3u);
+                } else {
+                    col = lut[mb | (e & 3u) << 10];
+                }
+            }
+        }
+        emit4<C>(H, acc, b, c, col, lane);
+    }
+    __syncwarp();
+    for (int base = x + 1; base < nL; base += 32) {
+        const int q = base + lane;
+        int col = kNone;
+        uint32_t c = 0;
+        if (q < nL) {
+            const uint32_t ec = La[q];
+            c = ec >> 2;
+            col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
+        }
+        emit4<C>(H, acc, b, c, col, lane);
+    }
+    __syncwarp();
+    clear_words(Bl, (x + 1) >> 4, (nL + 15) >> 4, lane);
+    if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    __syncwarp();
+}
+
+// The task (r, a = R[i]).  Ba/La (phase A) and, for heavy k = 4 tasks, codes must be ready.
+// NW == 1: one warp does everything in order.  NW > 1 (heavy): the CTA's warps take work
+// items from the shared counter *wctr (star chunks longest first, then b in R, then b in L_a).
+// Bb/Bl are this warp's scratch bitmaps (zero on entry and exit), H its histogram.
 template <int K, int NW>
-__device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R, int D,
-                           const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb, uint32_t *Bl, uint32_t *H,
-                           const uint8_t *codes,
-                           int w, int lane) {
+__device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
+                                           int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
+                                           uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, int w,
+                                           int lane) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
@@ -343,111 +461,34 @@ __device__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, 
             emit3<C>(H, acc, b, col, lane);
         }
         if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    } else if constexpr (NW == 1) {
+        for (int j = i + 1; !(g.skip & 2) && j < D; j++)
+            item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a, lane);
+        for (int x = 0; !(g.skip & 4) && x < nL; x++)
+            item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, lane);
     } else {
-        // mask: (r,a) | (r,b)<<2 | (r,c)<<4 | (a,b)<<6 | (a,c)<<8 | (b,c)<<10
-        if constexpr (NW > 1)
-            if (!(g.skip & 1)) star3_heavy<C, NW>(g, lut, r, i, R, D, Ba, codes, cra, a, H, w, lane);
-        for (int j = i + 1 + w; !(g.skip & 2) && j < D; j += NW) {                // b = R[j]
-            const uint32_t eb = R[j], b = eb >> 2;
-            const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
-            const int64_t b0 = g.off[b], b1 = g.off[b + 1];
-            // walk N(b): c in R after b -> Bb;  c in L_a -> Bl;  else "2+1" with c in L_b \ N(a)
-            for (int64_t base = b0; base < b1; base += 32) {
-                const int64_t p = base + lane;
-                int col = kNone;
-                uint32_t c = 0;
-                if (p < b1) {
-                    const uint32_t e = g.adj[p];
-                    c = e >> 2;
-                    if (c > r) {
-                        const int pos = find_rank(R, D, c);
-                        if (pos >= 0) {
-                            if (NW == 1 && pos > j) set2(Bb, pos, e & 3u);
-                        } else {
-                            const int q = find_rank(La, nL, c);
-                            if (q >= 0) set2(Bl, q, e & 3u);
-                            else col = lut[mb | (e & 3u) << 10];
-                        }
-                    }
-                }
-                emit4<C>(H, acc, b, c, col, lane);
+        const int nch = D - (i + 2) > 0 ? (D - (i + 2) + 63) / 64 : 0;
+        const int nB = D - 1 - i;
+        const int total = nch + nB + nL;
+        for (;;) {
+            int it = 0;
+            if (lane == 0) it = atomicAdd(wctr, 1);
+            it = __shfl_sync(kFull, it, 0);
+            if (it >= total) break;
+            if (it < nch) {
+                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, it, lane);
+            } else if (it < nch + nB) {
+                if (!(g.skip & 2))
+                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + (it - nch), R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
+                                       lane);
+            } else {
+                if (!(g.skip & 4)) item_b_in_La<C>(g, lut, r, it - nch - nB, R, D, La, nL, Bl, H, cra, a, lane);
             }
-            __syncwarp();
-            // "3": c in R after b (light tasks; heavy tasks ran star3_heavy)
-            for (int base = j + 1; NW == 1 && base < D; base += 32) {
-                const int p = base + lane;
-                int col = kNone;
-                uint32_t c = 0;
-                if (p < D) {
-                    const uint32_t ec = R[p];
-                    c = ec >> 2;
-                    col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
-                }
-                emit4<C>(H, acc, b, c, col, lane);
-            }
-            // "2+1": c in L_a
-            for (int base = 0; base < nL; base += 32) {
-                const int q = base + lane;
-                int col = kNone;
-                uint32_t c = 0;
-                if (q < nL) {
-                    const uint32_t ec = La[q];
-                    c = ec >> 2;
-                    col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
-                }
-                emit4<C>(H, acc, b, c, col, lane);
-            }
-            __syncwarp();
-            if (NW == 1) clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
-            clear_words(Bl, 0, (nL + 15) >> 4, lane);
-            if (g.big) flush_hist<C>(H, acc, r, a, lane);
-            __syncwarp();
-        }
-        for (int x = w; !(g.skip & 4) && x < nL; x += NW) {       // b = L_a[x]
-            const uint32_t eb = La[x], b = eb >> 2;
-            const uint32_t mb = cra | (eb & 3u) << 6;
-            const int64_t b0 = g.off[b], b1 = g.off[b + 1];
-            // walk N(b): c in R -> skip;  c in L_a after b -> Bl ("1+2");  else "1+1+1"
-            for (int64_t base = b0; base < b1; base += 32) {
-                const int64_t p = base + lane;
-                int col = kNone;
-                uint32_t c = 0;
-                if (p < b1) {
-                    const uint32_t e = g.adj[p];
-                    c = e >> 2;
-                    if (c > r && find_rank(R, D, c) < 0) {
-                        const int q = find_rank(La, nL, c);
-                        if (q >= 0) {
-                            if (q > x) set2(Bl, q, e & 3u);
-                        } else {
-                            col = lut[mb | (e & 3u) << 10];
-                        }
-                    }
-                }
-                emit4<C>(H, acc, b, c, col, lane);
-            }
-            __syncwarp();
-            // "1+2": c in L_a after b
-            for (int base = x + 1; base < nL; base += 32) {
-                const int q = base + lane;
-                int col = kNone;
-                uint32_t c = 0;
-                if (q < nL) {
-                    const uint32_t ec = La[q];
-                    c = ec >> 2;
-                    col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
-                }
-                emit4<C>(H, acc, b, c, col, lane);
-            }
-            __syncwarp();
-            clear_words(Bl, (x + 1) >> 4, (nL + 15) >> 4, lane);
-            if (g.big) flush_hist<C>(H, acc, r, a, lane);
-            __syncwarp();
         }
     }
 }
 
-template <int K>
+template <int K, bool HSMEM>
 __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo, int64_t hi,
                                                      unsigned long long *ctr, const uint8_t *__restrict__ lut_g) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
@@ -455,7 +496,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item;
-    __shared__ int s_nL;
+    __shared__ int s_nL, s_work;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
@@ -463,11 +504,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
 
     // ---------------- heavy phase: one CTA per task (r, a)
     {
-        uint32_t *hb = g.heavy_in_smem ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
+        // HSMEM: the heavy buffers are carved from shared memory (the compiler then emits LDS)
+        uint32_t *hb = HSMEM ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
         uint32_t *R = hb + L.R, *La = hb + L.La, *Ba = hb + L.Ba;
         uint32_t *Bl = hb + L.Bl + wid * L.lw;
         uint8_t *codes = reinterpret_cast<uint8_t *>(hb + L.Bb);   // heavy: per-task code bytes
-        if (!g.heavy_in_smem) {   // zero this CTA's global bitmaps once
+        if (!HSMEM) {   // zero this CTA's global bitmaps once
             for (int q = tid; q < L.Bl + kWarps * L.lw - L.Ba; q += kBlock) hb[L.Ba + q] = 0;
         }
         __syncthreads();
@@ -491,7 +533,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             }
             if (wid == 0) {
                 const int nL = build_a(g, r, R[i] >> 2, R, D, Ba, La, lane);
-                if (lane == 0) s_nL = nL;
+                if (lane == 0) {
+                    s_nL = nL;
+                    s_work = 0;
+                }
             }
             __syncthreads();
             const int nL = s_nL;
@@ -499,7 +544,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
                 __syncthreads();
             }
-            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, wid, lane);
+            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -540,7 +585,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     __syncwarp();
                 }
                 const int nL = build_a(g, r, a, R, D, Ba, La, lane);
-                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, 0, lane);
+                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
@@ -855,9 +900,10 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const char *force = getenv("VDMC_HEAVY_GLOBAL");
     const Layout L = make_layout((int)g->max_degree, C, heavy_in_smem, per_cta, force && force[0] == '1');
     const size_t smem = (size_t)L.total * 4;
-    VDMC_CUDA(cudaFuncSetAttribute(k_enum<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto kern = heavy_in_smem ? k_enum<K, true> : k_enum<K, false>;
+    VDMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_enum<K>, kBlock, smem));
+    VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
     const int grid = std::max(1, nsm * std::max(per_sm, 1));
     // global fallback scratch: heavy per-CTA buffers (huge degrees), light per-warp oversize L_a
     const int64_t per_warp = (int64_t)g->max_degree + (g->max_degree + 15) / 16 + 1;
@@ -902,7 +948,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
     if (hi > lo) {
-        k_enum<K><<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4);
+        kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4);
         VDMC_LAUNCH();
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[2], s));
