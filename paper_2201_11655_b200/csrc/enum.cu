@@ -65,6 +65,9 @@ struct Dev {
     int big;                                  // degrees so large a task could overflow u32 histograms
     int maxdeg;
     int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop
+    uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
+    int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
+    uint32_t ca_cap;
     const int64_t *__restrict__ hbase;        // heavy root -> segment of nr_off
     const int64_t *__restrict__ nr_off;       // induced adjacency of N+(r), position space
     const uint32_t *__restrict__ nr_adj;
@@ -423,6 +426,208 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
     __syncwarp();
 }
 
+// ------------------------------------------------------------------ "2+1" at heavy roots
+// For the task (r, x = R[i]) both kinds of "2+1" set containing x are enumerated with lanes =
+// c in L_x (two per lane: 64-wide chunks of L_x) and a warp-uniform walk over positions j of R:
+//   j > i:  {r, a = x, b = R[j], c}, c in L_a             (every j)
+//   j < i:  {r, a = R[j], b = x, c}, c in L_b \ N(a)      (only if R[j] is not adjacent to c)
+// Together these are exactly the "2+1" sets whose first or second depth-1 vertex is x, each
+// once (the set {r, a < b, c} is met in the task of a if c ~ a, else in the task of b).
+// code(R[j], c) comes from c's R-neighbour list, built per task in CTA scratch (ca_build).
+// As in the star loop, a plain set (no x-R[j] edge and no R[j]-c edge) has its class fixed by
+// c's code(x, c) and the iteration's code(r, R[j]): c and the pair (r, x) accumulate per-lane
+// 16-bit counters, R[j] gets popc(plain & M_k) per key k = code(x, c) from lanes 0..2, and
+// the remaining sets are classified one by one (cross_slow).
+constexpr int kCrossBlock = 2048;   // j-block length (< 2^16: the per-lane 16-bit counters)
+
+struct CrossC {
+    uint32_t c, cxc, npos, ncode, q, q1;
+    uint32_t f1A, f1B, f2A, f2B;   // plain sets for j > i / j < i: A = n(crj=1) | n(crj=2) << 16, B = n(crj=3)
+    int key;                       // code(x, c) - 1; 15 = no c
+};
+
+__device__ __forceinline__ void cross_c_next(const uint32_t *CA, CrossC &s) {
+    const uint32_t e = s.q < s.q1 ? CA[s.q] : 0xffffffffu;
+    s.npos = e >> 2;
+    s.ncode = e & 3u;
+}
+
+__device__ __forceinline__ void cross_c_init(CrossC &s, const uint32_t *La, int nL, const uint32_t *CAbeg,
+                                             const uint32_t *CAlen, const uint32_t *CA, int q, int j0) {
+    s.c = 0; s.cxc = 0; s.npos = 0x3fffffffu; s.ncode = 0; s.q = 0; s.q1 = 0;
+    s.f1A = 0; s.f1B = 0; s.f2A = 0; s.f2B = 0; s.key = 15;
+    if (q < nL) {
+        const uint32_t e = La[q];
+        s.c = e >> 2;
+        s.cxc = e & 3u;
+        s.key = (int)s.cxc - 1;
+        s.q = CAbeg[q];
+        s.q1 = s.q + CAlen[q];
+        cross_c_next(CA, s);
+        while (s.npos < (uint32_t)j0) {
+            s.q++;
+            cross_c_next(CA, s);
+        }
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void cross_c_flush(const Dev &g, CrossC &s, const uint8_t *lut, uint32_t *H, uint32_t cra) {
+    if (s.key == 15) return;
+    const uint32_t n1[3] = {s.f1A & 0xffffu, s.f1A >> 16, s.f1B};
+    const uint32_t n2[3] = {s.f2A & 0xffffu, s.f2A >> 16, s.f2B};
+#pragma unroll
+    for (uint32_t crj = 1; crj <= 3; crj++) {
+        if (n1[crj - 1]) {   // (r, x, R[j], c)
+            const int col = lut[cra | crj << 2 | s.cxc << 8];
+            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n1[crj - 1]);
+            atomicAdd(H + col, n1[crj - 1]);
+        }
+        if (n2[crj - 1]) {   // (r, R[j], x, c)
+            const int col = lut[crj | cra << 2 | s.cxc << 10];
+            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n2[crj - 1]);
+            atomicAdd(H + col, n2[crj - 1]);
+        }
+    }
+    s.f1A = 0; s.f1B = 0; s.f2A = 0; s.f2B = 0;
+}
+
+// a non-plain set: PART 1 (j > i) with an x-R[j] or R[j]-c edge, PART 2 (j < i) with an
+// x-R[j] edge (and no R[j]-c edge)
+template <int C, int PART>
+__device__ __forceinline__ void cross_slow(const Dev &g, const CrossC &s, const uint8_t *lut, uint32_t *H, uint32_t ub,
+                                           uint32_t cra, uint32_t b, bool hit) {
+    const uint32_t crj = ub & 3u, cxj = ub >> 2;   // code(r, R[j]), code(x, R[j])
+    int col;
+    if (PART == 1) {
+        const uint32_t cjc = hit ? swap2(s.ncode) : 0u;   // the entry holds code(c, R[j])
+        col = lut[cra | crj << 2 | cxj << 6 | s.cxc << 8 | cjc << 10];
+    } else {
+        col = lut[crj | cra << 2 | swap2(cxj) << 6 | s.cxc << 10];
+    }
+    atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
+    atomicAdd(g.acc + (size_t)b * C + col, 1ull);
+    atomicAdd(H + col, 1u);
+}
+
+template <int C, int PART>
+__device__ __forceinline__ void cross_run(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
+                                          const uint8_t *codes, const uint32_t *CA, CrossC &s0, CrossC &s1,
+                                          unsigned M0, unsigned M1, uint32_t cra, int j0, int j1, int lane) {
+    const uint32_t kc = (uint32_t)lane + 1u;   // lanes 0..2 own key code(x, c) = lane + 1
+    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    for (int j = j0; j < j1; j++) {
+        const uint32_t ub = codes[j];
+        const uint32_t crj = ub & 3u;
+        const bool cz = ub < 4u;                    // no x-R[j] edge
+        const uint32_t incA = crj == 1u ? 1u : (crj == 2u ? 0x10000u : 0u);
+        const uint32_t incB = crj == 3u ? 1u : 0u;
+        const bool h0 = s0.npos == (uint32_t)j, h1 = s1.npos == (uint32_t)j;
+        const bool pl0 = vc0 && !h0 && cz, pl1 = vc1 && !h1 && cz;
+        if (PART == 1) {
+            s0.f1A += pl0 ? incA : 0u;
+            s0.f1B += pl0 ? incB : 0u;
+            s1.f1A += pl1 ? incA : 0u;
+            s1.f1B += pl1 ? incB : 0u;
+        } else {
+            s0.f2A += pl0 ? incA : 0u;
+            s0.f2B += pl0 ? incB : 0u;
+            s1.f2A += pl1 ? incA : 0u;
+            s1.f2B += pl1 ? incB : 0u;
+        }
+        const unsigned bm0 = __ballot_sync(kFull, pl0), bm1 = __ballot_sync(kFull, pl1);
+        const unsigned cnt = __popc(bm0 & M0) + __popc(bm1 & M1);   // lanes >= 3 have M = 0
+        if (cnt) {
+            const int col = PART == 1 ? lut[cra | crj << 2 | kc << 8] : lut[crj | cra << 2 | kc << 10];
+            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cnt);
+        }
+        const bool sl0 = vc0 && !pl0 && (PART == 1 || !h0), sl1 = vc1 && !pl1 && (PART == 1 || !h1);
+        if (__any_sync(kFull, sl0 || sl1 || h0 || h1)) {   // rare, warp-uniform
+            const uint32_t b = R[j] >> 2;
+            if (sl0) cross_slow<C, PART>(g, s0, lut, H, ub, cra, b, h0);
+            if (sl1) cross_slow<C, PART>(g, s1, lut, H, ub, cra, b, h1);
+            if (h0) { s0.q++; cross_c_next(CA, s0); }
+            if (h1) { s1.q++; cross_c_next(CA, s1); }
+        }
+    }
+}
+
+// item (k, jb): c = L_x[64k .. 64k+63], positions j in block jb of length kCrossBlock
+template <int C>
+__device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
+                                           int D, const uint8_t *codes, const uint32_t *La, int nL,
+                                           const uint32_t *CAbeg, const uint32_t *CAlen, const uint32_t *CA,
+                                           uint32_t cra, uint32_t a, uint32_t *H, int k, int jb, int lane) {
+    const int j0 = jb * kCrossBlock, j1 = min(D, j0 + kCrossBlock);
+    CrossC s0, s1;
+    cross_c_init(s0, La, nL, CAbeg, CAlen, CA, 64 * k + lane, j0);
+    cross_c_init(s1, La, nL, CAbeg, CAlen, CA, 64 * k + 32 + lane, j0);
+    unsigned M0 = 0, M1 = 0;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const unsigned m0 = __ballot_sync(kFull, s0.key == q), m1 = __ballot_sync(kFull, s1.key == q);
+        if (lane == q) { M0 = m0; M1 = m1; }
+    }
+    cross_run<C, 2>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j0, min(j1, i), lane);
+    cross_run<C, 1>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, max(j0, i + 1), j1, lane);
+    cross_c_flush<C>(g, s0, lut, H, cra);
+    cross_c_flush<C>(g, s1, lut, H, cra);
+    if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
+    __syncwarp();
+}
+
+// c's R-neighbour lists (positions ascending, x = R[i] excluded, code(c, R[pos])) for every c
+// in L_x, into the CTA scratch; each warp walks the lists of its c's twice (count, write).
+// Returns false if they do not fit (the task then falls back to item_b_in_R).
+template <int NW>
+__device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const uint32_t *R, int D,
+                                         const uint32_t *La, int nL, uint32_t *CAbeg, uint32_t *CAlen, uint32_t *CA,
+                                         int *s_ca, int w, int lane) {
+    for (int q = w; q < nL; q += NW) {
+        const uint32_t c = La[q] >> 2;
+        const int64_t c0 = g.off[c], c1 = g.off[c + 1];
+        int cnt = 0;
+        for (int64_t base = c0; base < c1; base += 32) {
+            const int64_t p = base + lane;
+            bool keep = false;
+            if (p < c1) {
+                const uint32_t y = g.adj[p] >> 2;
+                if (y > r) {
+                    const int pos = find_rank(R, D, y);
+                    keep = pos >= 0 && pos != i;
+                }
+            }
+            cnt += __popc(__ballot_sync(kFull, keep));
+        }
+        int beg = 0;
+        if (lane == 0) beg = atomicAdd(s_ca, cnt);
+        beg = __shfl_sync(kFull, beg, 0);
+        if (lane == 0) {
+            CAbeg[q] = (uint32_t)beg;
+            CAlen[q] = (uint32_t)cnt;
+        }
+        if (beg + cnt > (int)g.ca_cap) continue;
+        int k = 0;
+        for (int64_t base = c0; base < c1; base += 32) {
+            const int64_t p = base + lane;
+            int pos = -1;
+            uint32_t e = 0;
+            if (p < c1) {
+                e = g.adj[p];
+                if ((e >> 2) > r) {
+                    pos = find_rank(R, D, e >> 2);
+                    if (pos == i) pos = -1;
+                }
+            }
+            const unsigned bal = __ballot_sync(kFull, pos >= 0);
+            if (pos >= 0) CA[beg + k + __popc(bal & ((1u << lane) - 1u))] = ((uint32_t)pos << 2) | (e & 3u);
+            k += __popc(bal);
+        }
+    }
+    __syncthreads();
+    return *s_ca <= (int)g.ca_cap;
+}
+
 // The task (r, a = R[i]).  Ba/La (phase A) and, for heavy k = 4 tasks, codes must be ready.
 // NW == 1: one warp does everything in order.  NW > 1 (heavy): the CTA's warps take work
 // items from the shared counter *wctr (star chunks longest first, then b in R, then b in L_a).
@@ -430,8 +635,8 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
 template <int K, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
-                                           uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, int w,
-                                           int lane) {
+                                           uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
+                                           int *s_ca, int w, int lane) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
@@ -467,8 +672,11 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         for (int x = 0; !(g.skip & 4) && x < nL; x++)
             item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, lane);
     } else {
-        const int nch = D - (i + 2) > 0 ? (D - (i + 2) + 63) / 64 : 0;
-        const int nB = D - 1 - i;
+        uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
+        const bool cross = ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
+        const int nch = D - (i + 2) > 0 ? (D - (i + 2) + 63) / 64 : 0;          // star chunks
+        const int nck = (nL + 63) / 64, njb = (D + kCrossBlock - 1) / kCrossBlock;
+        const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
         const int total = nch + nB + nL;
         for (;;) {
             int it = 0;
@@ -478,9 +686,13 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             if (it < nch) {
                 if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, it, lane);
             } else if (it < nch + nB) {
-                if (!(g.skip & 2))
-                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + (it - nch), R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
-                                       lane);
+                const int b_it = it - nch;
+                if (g.skip & 2) continue;
+                if (cross)
+                    cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, b_it / njb,
+                                  b_it % njb, lane);
+                else
+                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a, lane);
             } else {
                 if (!(g.skip & 4)) item_b_in_La<C>(g, lut, r, it - nch - nB, R, D, La, nL, Bl, H, cra, a, lane);
             }
@@ -496,7 +708,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item;
-    __shared__ int s_nL, s_work;
+    __shared__ int s_nL, s_work, s_ca;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
@@ -536,6 +748,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 if (lane == 0) {
                     s_nL = nL;
                     s_work = 0;
+                    s_ca = 0;
                 }
             }
             __syncthreads();
@@ -544,7 +757,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
                 __syncthreads();
             }
-            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work, wid, lane);
+            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -585,7 +799,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     __syncwarp();
                 }
                 const int nL = build_a(g, r, a, R, D, Ba, La, lane);
-                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, 0, lane);
+                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, 0,
+                                 lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
@@ -907,7 +1122,9 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const int grid = std::max(1, nsm * std::max(per_sm, 1));
     // global fallback scratch: heavy per-CTA buffers (huge degrees), light per-warp oversize L_a
     const int64_t per_warp = (int64_t)g->max_degree + (g->max_degree + 15) / 16 + 1;
-    const size_t need = (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
+    const uint32_t ca_cap = 1u << 16;
+    const int64_t per_cta_ca = 2 * (int64_t)std::max<int64_t>(g->max_degree, 1) + ca_cap;
+    const size_t need = (size_t)grid * (per_cta + (int64_t)kWarps * per_warp + per_cta_ca);
     if (g->lscratch_elems < need) {
         if (g->lscratch) cudaFree(g->lscratch);
         g->lscratch = nullptr;
@@ -939,6 +1156,9 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.acc = (unsigned long long *)g->acc;
     d.gheavy = g->lscratch;
     d.glight = g->lscratch + (size_t)grid * per_cta;
+    d.gca = g->lscratch + (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
+    d.gca_per_cta = per_cta_ca;
+    d.ca_cap = ca_cap;
     d.gheavy_per_cta = per_cta;
     d.glight_per_warp = per_warp;
     d.heavy_in_smem = heavy_in_smem ? 1 : 0;
