@@ -28,6 +28,29 @@ vdmc_status fail(vdmc_status st, const char *fmt, ...) {
 
 void count_launch(int n) { g_launches += n; }
 
+cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static bool configured[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 64 && !configured[dev]) {
+            cudaMemPool_t pool;
+            if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+            uint64_t thr = ~0ull;
+            if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
+            configured[dev] = true;
+        }
+    }
+    return cudaMallocAsync(p, bytes ? bytes : 1, s);
+}
+
+void dfree(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 // ------------------------------------------------------------ class table
 // Paper index (Fig. 1): the adjacency matrix read row by row without the
 // diagonal; the first entry is the most significant bit.  Class = minimum index over all
@@ -332,8 +355,8 @@ void vdmc_free_graph(vdmc_graph *g) {
     void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->acc,
                     g->lscratch, g->ctr, g->lut3, g->lut4, g->cost, g->heavy_task, g->light_root,
                     g->hroots, g->hbase, g->nr_off, g->nr_adj};
-    for (void *p : ptrs)
-        if (p) cudaFree(p);
+    for (void *p : ptrs) dfree(p, nullptr);
+    cudaStreamSynchronize(nullptr);
     for (auto &e : g->ev)
         if (e) cudaEventDestroy(e);
     delete g;

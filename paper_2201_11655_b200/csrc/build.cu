@@ -218,7 +218,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     const int64_t nnz = g->nnz;
 
     // ---- S2: order
-    VDMC_CUDA(cudaMalloc(&g->order, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+    VDMC_CUDA(dalloc((void **)&g->order, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
     if (n > 0) {
         if (h_rank) {
             VDMC_CUDA(cudaMemcpyAsync(rank, h_rank, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
@@ -243,10 +243,10 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     }
 
     // ---- S2: relabel + sort + CSR
-    VDMC_CUDA(cudaMalloc(&g->off, sizeof(int64_t) * (n + 1)));
-    VDMC_CUDA(cudaMalloc(&g->split, sizeof(int64_t) * std::max<int64_t>(n, 1)));
-    VDMC_CUDA(cudaMalloc(&g->adj, sizeof(uint32_t) * std::max<int64_t>(nnz, 1)));
-    VDMC_CUDA(cudaMalloc(&g->tfirst, sizeof(int64_t) * (n + 1)));
+    VDMC_CUDA(dalloc((void **)&g->off, sizeof(int64_t) * (n + 1), s));
+    VDMC_CUDA(dalloc((void **)&g->split, sizeof(int64_t) * std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(dalloc((void **)&g->adj, sizeof(uint32_t) * std::max<int64_t>(nnz, 1), s));
+    VDMC_CUDA(dalloc((void **)&g->tfirst, sizeof(int64_t) * (n + 1), s));
     VDMC_CUDA(cudaMemsetAsync(g->off, 0, sizeof(int64_t) * (n + 1), s));
     VDMC_CUDA(cudaMemsetAsync(g->tfirst, 0, sizeof(int64_t) * (n + 1), s));
     if (nnz > 0) {
@@ -293,7 +293,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         g->max_degree = hmax;
     }
     g->ntasks = nnz / 2;
-    VDMC_CUDA(cudaMalloc(&g->task_root, sizeof(int32_t) * std::max<int64_t>(g->ntasks, 1)));
+    VDMC_CUDA(dalloc((void **)&g->task_root, sizeof(int32_t) * std::max<int64_t>(g->ntasks, 1), s));
     if (g->ntasks > 0) {
         k_task_root<<<grid_for(n * 32), kThreads, 0, s>>>(n, g->tfirst, g->task_root);
         VDMC_LAUNCH();

@@ -945,24 +945,24 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
 
 }  // namespace
 
-vdmc_status ensure_acc(vdmc_graph *g, int k) {
+vdmc_status ensure_acc(vdmc_graph *g, int k, cudaStream_t s) {
     const int C = num_classes(k);
     const size_t need = (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t);
     if (g->acc_bytes < need) {
-        if (g->acc) cudaFree(g->acc);
+        dfree(g->acc, s);
         g->acc = nullptr;
         g->acc_bytes = 0;
-        VDMC_CUDA(cudaMalloc(&g->acc, need));
+        VDMC_CUDA(dalloc((void **)&g->acc, need, s));
         g->acc_bytes = need;
     }
-    if (!g->ctr) VDMC_CUDA(cudaMalloc(&g->ctr, 4 * sizeof(unsigned long long)));
+    if (!g->ctr) VDMC_CUDA(dalloc((void **)&g->ctr, 4 * sizeof(unsigned long long), s));
     if (!g->lut3) {
-        VDMC_CUDA(cudaMalloc(&g->lut3, 64));
-        VDMC_CUDA(cudaMemcpy(g->lut3, host_lut(3), 64, cudaMemcpyHostToDevice));
+        VDMC_CUDA(dalloc((void **)&g->lut3, 64, s));
+        VDMC_CUDA(cudaMemcpyAsync(g->lut3, host_lut(3), 64, cudaMemcpyHostToDevice, s));
     }
     if (!g->lut4) {
-        VDMC_CUDA(cudaMalloc(&g->lut4, 4096));
-        VDMC_CUDA(cudaMemcpy(g->lut4, host_lut(4), 4096, cudaMemcpyHostToDevice));
+        VDMC_CUDA(dalloc((void **)&g->lut4, 4096, s));
+        VDMC_CUDA(cudaMemcpyAsync(g->lut4, host_lut(4), 4096, cudaMemcpyHostToDevice, s));
     }
     return VDMC_OK;
 }
@@ -977,8 +977,8 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
     VDMC_CUDA(cudaMallocAsync(&fl, std::max<int64_t>(n, 1), s));
     VDMC_CUDA(cudaMallocAsync(&ft, std::max<int64_t>(T, 1), s));
     VDMC_CUDA(cudaMallocAsync(&nsel, sizeof(int64_t) * 2, s));
-    if (!g->light_root) VDMC_CUDA(cudaMalloc(&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1)));
-    if (!g->heavy_task) VDMC_CUDA(cudaMalloc(&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1)));
+    if (!g->light_root) VDMC_CUDA(dalloc((void **)&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    if (!g->heavy_task) VDMC_CUDA(dalloc((void **)&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1), s));
     int64_t hn[2] = {0, 0};
     if (n > 0 && T > 0) {
         k_root_flags<<<148 * 8, 256, 0, s>>>(n, g->off, g->tfirst, fh, fl);
@@ -999,8 +999,8 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
     }
     // heavy roots (rank order) and the induced adjacency of each one's N+(r)
     int64_t nhr = 0;
-    if (!g->hroots) VDMC_CUDA(cudaMalloc(&g->hroots, sizeof(int32_t) * std::max<int64_t>(n, 1)));
-    if (!g->hbase) VDMC_CUDA(cudaMalloc(&g->hbase, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+    if (!g->hroots) VDMC_CUDA(dalloc((void **)&g->hroots, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    if (!g->hbase) VDMC_CUDA(dalloc((void **)&g->hbase, sizeof(int64_t) * std::max<int64_t>(n, 1), s));
     if (n > 0 && T > 0) {
         thrust::counting_iterator<int32_t> ids(0);
         size_t tb = 0;
@@ -1037,8 +1037,8 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         int64_t *cnt = nullptr;
         VDMC_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (sumD + 1), s));
         VDMC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (sumD + 1), s));
-        if (g->nr_off) cudaFree(g->nr_off);
-        VDMC_CUDA(cudaMalloc(&g->nr_off, sizeof(int64_t) * (sumD + 1)));
+        dfree(g->nr_off, s);
+        VDMC_CUDA(dalloc((void **)&g->nr_off, sizeof(int64_t) * (sumD + 1), s));
         const int cap = (int)std::min<int64_t>(g->max_degree, 12288);
         const size_t sm = (size_t)std::max(cap, 1) * 4;
         VDMC_CUDA(cudaFuncSetAttribute(k_nr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1055,8 +1055,8 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         count_launch(2);
         VDMC_CUDA(cudaMemcpyAsync(&g->nr_total, g->nr_off + sumD, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
-        if (g->nr_adj) cudaFree(g->nr_adj);
-        VDMC_CUDA(cudaMalloc(&g->nr_adj, sizeof(uint32_t) * std::max<int64_t>(g->nr_total, 1)));
+        dfree(g->nr_adj, s);
+        VDMC_CUDA(dalloc((void **)&g->nr_adj, sizeof(uint32_t) * std::max<int64_t>(g->nr_total, 1), s));
         k_nr<true><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, nullptr, g->nr_off,
                                            g->nr_adj, g->ctr + 3, cap);
         VDMC_LAUNCH();
@@ -1078,7 +1078,7 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
 
 vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t s) {
     if (g->cost && g->cost_k == k) return VDMC_OK;
-    if (!g->cost) VDMC_CUDA(cudaMalloc(&g->cost, sizeof(int64_t) * std::max<int64_t>(g->ntasks, 1)));
+    if (!g->cost) VDMC_CUDA(dalloc((void **)&g->cost, sizeof(int64_t) * std::max<int64_t>(g->ntasks, 1), s));
     if (g->ntasks > 0) {
         int64_t *raw = nullptr;
         VDMC_CUDA(cudaMallocAsync(&raw, sizeof(int64_t) * g->ntasks, s));
@@ -1126,10 +1126,10 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const int64_t per_cta_ca = 2 * (int64_t)std::max<int64_t>(g->max_degree, 1) + ca_cap;
     const size_t need = (size_t)grid * (per_cta + (int64_t)kWarps * per_warp + per_cta_ca);
     if (g->lscratch_elems < need) {
-        if (g->lscratch) cudaFree(g->lscratch);
+        dfree(g->lscratch, s);
         g->lscratch = nullptr;
         g->lscratch_elems = 0;
-        VDMC_CUDA(cudaMalloc(&g->lscratch, need * sizeof(uint32_t)));
+        VDMC_CUDA(dalloc((void **)&g->lscratch, need * sizeof(uint32_t), s));
         g->lscratch_elems = need;
     }
     VDMC_CUDA(cudaMemsetAsync(g->acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
@@ -1184,7 +1184,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
 }
 
 vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi, cudaStream_t s) {
-    vdmc_status st = ensure_acc(g, k);
+    vdmc_status st = ensure_acc(g, k, s);
     if (st) return st;
     return k == 3 ? run<3>(g, counts, lo, hi, s) : run<4>(g, counts, lo, hi, s);
 }

@@ -14,6 +14,11 @@ namespace vdmc {
 void set_error(const std::string &msg);
 vdmc_status fail(vdmc_status st, const char *fmt, ...);
 void count_launch(int n = 1);
+// Device memory: stream-ordered allocations from the device's default pool, which retains
+// freed memory (release threshold = max), so building and counting again reuses it instead of
+// paying cudaMalloc/cudaFree (page mapping of GB-sized count matrices) every call.
+cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s);
+void dfree(void *p, cudaStream_t s);
 
 #define VDMC_CUDA(call)                                                                  \
     do {                                                                                 \
@@ -93,7 +98,7 @@ struct vdmc_graph {
 namespace vdmc {
 vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst,
                          const int32_t *h_rank, int device, cudaStream_t stream, vdmc_graph *g);
-vdmc_status ensure_acc(vdmc_graph *g, int k);
+vdmc_status ensure_acc(vdmc_graph *g, int k, cudaStream_t s);
 vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t stream);
 vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi,
                          cudaStream_t stream);
