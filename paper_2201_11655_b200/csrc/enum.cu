@@ -84,7 +84,9 @@ struct Layout {
 constexpr int kLW = kLightDeg;               // light list capacity
 constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 // per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
-constexpr int kLightWords = 2 * kLW + 3 * kLB;
+constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
+constexpr int kLcap = 320;                   // light: staged list entries (R's lists, L_a's lists)
+constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + 2 * kLcap;
 
 __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x) {
     // position of vertex x in the sorted entry list S[0..len), or -1
@@ -150,18 +152,87 @@ __device__ __forceinline__ void clear_words(uint32_t *B, int w0, int w1, int lan
     for (int w = w0 + lane; w < w1; w += 32) B[w] = 0;
 }
 
+// A vertex's adjacency list: in global memory, or staged in the warp's shared memory.
+struct List {
+    const uint32_t *p;
+    int len;
+};
+__device__ __forceinline__ List glist(const Dev &g, uint32_t v) {
+    const int64_t o = g.off[v];
+    return List{g.adj + o, (int)(g.off[v + 1] - o)};
+}
+
+// Copy the lists of the m vertices V[q] >> 2 (q < m) into B (capacity cap), S[q] = start of
+// q's list, S[m] = total, O[q] = its global offset.  One flattened pass, every load
+// independent (memory-level parallelism instead of one dependent chain per list).
+// Returns false (and stages nothing) if m > smax or the lists exceed cap.  One warp.
+__device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S, uint32_t *O, int smax, uint32_t *B,
+                             int cap, int lane) {
+    if (m > smax) return false;
+    int total = 0;
+    for (int b0 = 0; b0 < m; b0 += 32) {
+        const int q = b0 + lane;
+        int len = 0;
+        uint32_t o = 0;
+        if (q < m) {
+            const uint32_t v = V[q] >> 2;
+            const int64_t x0 = g.off[v];
+            o = (uint32_t)x0;
+            len = (int)(g.off[v + 1] - x0);
+        }
+        int inc = len;   // inclusive warp scan
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += y;
+        }
+        if (q < m) {
+            S[q] = (uint32_t)(total + inc - len);
+            O[q] = o;
+        }
+        total += __shfl_sync(kFull, inc, 31);
+    }
+    __syncwarp();
+    if (total > cap) return false;
+    if (lane == 0) S[m] = (uint32_t)total;
+    __syncwarp();
+#pragma unroll 4
+    for (int f = lane; f < total; f += 32) {
+        int lo = 0, hi = m;   // last q with S[q] <= f
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)S[mid] <= f) lo = mid;
+            else hi = mid;
+        }
+        B[f] = g.adj[(int64_t)O[lo] + (f - (int)S[lo])];
+    }
+    __syncwarp();
+    return true;
+}
+
+// Lists staged in a light warp's shared memory (gather_lists), else read from global memory.
+struct Staged {
+    const uint32_t *RL, *RS;   // lists of the vertices of R     (valid if rok)
+    const uint32_t *LL, *LS;   // lists of the vertices of L_a   (valid if lok)
+    bool rok, lok;
+};
+__device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, const uint32_t *B, const uint32_t *S,
+                                        bool ok) {
+    if (ok) return List{B + S[q], (int)(S[q + 1] - S[q])};
+    return glist(g, V[q] >> 2);
+}
+
 // Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
-// Run by one warp.  Returns |L_a|.
-__device__ int build_a(const Dev &g, uint32_t r, uint32_t a, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
+// al = a's list.  Run by one warp.  Returns |L_a|.
+__device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
                        int lane) {
-    const int64_t a0 = g.off[a], a1 = g.off[a + 1];
     int nL = 0;
-    for (int64_t base = a0; base < a1; base += 32) {
-        const int64_t p = base + lane;
+    for (int base = 0; base < al.len; base += 32) {
+        const int p = base + lane;
         bool keep = false;
         uint32_t e = 0;
-        if (p < a1) {
-            e = g.adj[p];
+        if (p < al.len) {
+            e = al.p[p];
             const uint32_t x = e >> 2;
             if (x > r) {
                 const int pos = find_rank(R, D, x);
@@ -322,17 +393,16 @@ template <int C, int NW>
 __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, uint32_t r, int i, int j,
                                             const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La, int nL,
                                             uint32_t *Bb, uint32_t *Bl, uint32_t *H, uint32_t cra, uint32_t a,
-                                            int lane) {
+                                            List bl, int lane) {
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t eb = R[j], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
-    const int64_t b0 = g.off[b], b1 = g.off[b + 1];
-    for (int64_t base = b0; base < b1; base += 32) {
-        const int64_t p = base + lane;
+    for (int base = 0; base < bl.len; base += 32) {
+        const int p = base + lane;
         int col = kNone;
         uint32_t c = 0;
-        if (p < b1) {
-            const uint32_t e = g.adj[p];
+        if (p < bl.len) {
+            const uint32_t e = bl.p[p];
             c = e >> 2;
             if (c > r) {
                 const int pos = find_rank(R, D, c);
@@ -385,17 +455,16 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
 template <int C>
 __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, uint32_t r, int x, const uint32_t *R,
                                              int D, const uint32_t *La, int nL, uint32_t *Bl, uint32_t *H,
-                                             uint32_t cra, uint32_t a, int lane) {
+                                             uint32_t cra, uint32_t a, List bl, int lane) {
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t eb = La[x], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 6;
-    const int64_t b0 = g.off[b], b1 = g.off[b + 1];
-    for (int64_t base = b0; base < b1; base += 32) {
-        const int64_t p = base + lane;
+    for (int base = 0; base < bl.len; base += 32) {
+        const int p = base + lane;
         int col = kNone;
         uint32_t c = 0;
-        if (p < b1) {
-            const uint32_t e = g.adj[p];
+        if (p < bl.len) {
+            const uint32_t e = bl.p[p];
             c = e >> 2;
             if (c > r && find_rank(R, D, c) < 0) {
                 const int q = find_rank(La, nL, c);
@@ -636,7 +705,7 @@ template <int K, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
-                                           int *s_ca, int w, int lane) {
+                                           int *s_ca, const Staged *st, int w, int lane) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
@@ -668,9 +737,11 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         if (g.big) flush_hist<C>(H, acc, r, a, lane);
     } else if constexpr (NW == 1) {
         for (int j = i + 1; !(g.skip & 2) && j < D; j++)
-            item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a, lane);
+            item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a,
+                              list_at(g, R, j, st->RL, st->RS, st->rok), lane);
         for (int x = 0; !(g.skip & 4) && x < nL; x++)
-            item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, lane);
+            item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, list_at(g, La, x, st->LL, st->LS, st->lok),
+                            lane);
     } else {
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
@@ -692,9 +763,12 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                     cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, b_it / njb,
                                   b_it % njb, lane);
                 else
-                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a, lane);
+                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
+                                       glist(g, R[i + 1 + b_it] >> 2), lane);
             } else {
-                if (!(g.skip & 4)) item_b_in_La<C>(g, lut, r, it - nch - nB, R, D, La, nL, Bl, H, cra, a, lane);
+                if (!(g.skip & 4))
+                    item_b_in_La<C>(g, lut, r, it - nch - nB, R, D, La, nL, Bl, H, cra, a,
+                                    glist(g, La[it - nch - nB] >> 2), lane);
             }
         }
     }
@@ -744,7 +818,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
             }
             if (wid == 0) {
-                const int nL = build_a(g, r, R[i] >> 2, R, D, Ba, La, lane);
+                const int nL = build_a(g, r, glist(g, R[i] >> 2), R, D, Ba, La, lane);
                 if (lane == 0) {
                     s_nL = nL;
                     s_work = 0;
@@ -758,7 +832,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
             }
             task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, wid, lane);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, nullptr, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -773,7 +847,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     {
         uint32_t *lw = sm + L.light + wid * kLightWords;
         uint32_t *R = lw, *Las = lw + kLW, *Ba = lw + 2 * kLW, *Bb = Ba + kLB, *Bls = Bb + kLB;
+        uint32_t *RS = Bls + kLB, *RO = RS + kSmax + 1, *LS = RO + kSmax, *LO = LS + kSmax + 1;
+        uint32_t *RL = LO + kSmax, *LL = RL + kLcap;   // staged adjacency lists
         uint32_t *gw = g.glight + ((int64_t)blockIdx.x * kWarps + wid) * g.glight_per_warp;   // oversize L_a
+        Staged st{RL, RS, LL, LS, false, false};
         for (;;) {
             unsigned long long x = 0;
             if (lane == 0) x = atomicAdd(ctr + 1, 1ull);
@@ -787,20 +864,22 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int D = (int)(g.off[r + 1] - rs);
             for (int q = lane; q < D; q += 32) R[q] = g.adj[rs + q];
             __syncwarp();
+            st.rok = gather_lists(g, R, D, RS, RO, kSmax, RL, kLcap, lane);   // lists of R, once per root
             for (int64_t t = ta; t < tb; t++) {
                 const int i = (int)(t - t0);
                 const uint32_t a = R[i] >> 2;
-                const int da = (int)(g.off[a + 1] - g.off[a]);
+                const List al = list_at(g, R, i, RL, RS, st.rok);
                 uint32_t *La = Las, *Bl = Bls;
-                if (da > kLW) {   // only with a user-given order: lists longer than the smem slots
+                if (al.len > kLW) {   // only with a user-given order: lists longer than the smem slots
                     La = gw;
                     Bl = gw + g.maxdeg;
-                    clear_words(Bl, 0, (da + 15) >> 4, lane);
+                    clear_words(Bl, 0, (al.len + 15) >> 4, lane);
                     __syncwarp();
                 }
-                const int nL = build_a(g, r, a, R, D, Ba, La, lane);
-                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, 0,
-                                 lane);
+                const int nL = build_a(g, r, al, R, D, Ba, La, lane);
+                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kLcap, lane);
+                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
+                                 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();

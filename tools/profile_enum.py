@@ -18,3 +18,5 @@ for _ in range(reps):
     out = g.count(k)
     torch.cuda.synchronize()
     print(name, k, g.timings(), flush=True)
+tot = int(out.sum().item())
+print("sets", tot // k)
