@@ -44,7 +44,7 @@ namespace {
 
 constexpr int kWarps = 16;            // warps per CTA
 constexpr int kBlock = kWarps * 32;
-constexpr int kLightDeg = 256;        // light root: G_U degree <= this
+constexpr int kLightDeg = 128;        // light root: G_U degree <= this (measured best of 64/128/256)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 

@@ -1,4 +1,5 @@
-"""Run one BASELINE config's count a few times (for ncu): python tools/profile_enum.py cfg3 4 [reps]"""
+"""Run one BASELINE config's count a few times (for ncu / quick timing):
+python tools/profile_enum.py cfg3 4 [reps] [scale]"""
 import os
 import sys
 
@@ -17,6 +18,6 @@ g.set_profiling(True)
 for _ in range(reps):
     out = g.count(k)
     torch.cuda.synchronize()
-    print(name, k, g.timings(), flush=True)
-tot = int(out.sum().item())
-print("sets", tot // k)
+t = g.timings()
+print(f"{name} k={k} enum_ms={t['enum']:.2f} plan_ms={t['plan']:.2f} build_ms={t['build']:.2f} "
+      f"sets={int(out.sum().item()) // k}", flush=True)
