@@ -77,6 +77,7 @@ struct Dev {
 struct Layout {
     int R, La, Ba, Bb, Bl;        // heavy: R[maxdeg], La[maxdeg], Ba[bw], Bb[kWarps][bw], Bl[kWarps][lw]
     int bw, lw;                   // bitmap words for R positions / L positions
+    int AP;                       // heavy: positions of R adjacent to a [kAPcap]
     int hist;                     // per-warp u32 histograms [kWarps][C]
     int light;                    // light region: per warp kLightWords
     int total;                    // words
@@ -84,6 +85,7 @@ struct Layout {
 constexpr int kLW = kLightDeg;               // light list capacity
 constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 // per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
+constexpr int kAPcap = 1024;                 // heavy: positions of R adjacent to a, kept for the fast loops
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
 constexpr int kLcap = 320;                   // light: staged list entries (R's lists, L_a's lists)
 constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + 2 * kLcap;
@@ -225,17 +227,19 @@ __device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, 
 // Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
 // al = a's list.  Run by one warp.  Returns |L_a|.
 __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
-                       int lane) {
-    int nL = 0;
+                       int lane, uint32_t *AP = nullptr, int *nap = nullptr) {
+    // AP (optional): the positions of R adjacent to a, ascending (*nap = their number)
+    int nL = 0, nA = 0;
     for (int base = 0; base < al.len; base += 32) {
         const int p = base + lane;
         bool keep = false;
+        int pos = -1;
         uint32_t e = 0;
         if (p < al.len) {
             e = al.p[p];
             const uint32_t x = e >> 2;
             if (x > r) {
-                const int pos = find_rank(R, D, x);
+                pos = find_rank(R, D, x);
                 if (pos >= 0) set2(Ba, pos, e & 3u);
                 else keep = true;
             }
@@ -243,8 +247,15 @@ __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int
         const unsigned bal = __ballot_sync(kFull, keep);
         if (keep) La[nL + __popc(bal & ((1u << lane) - 1u))] = e;
         nL += __popc(bal);
+        if (AP) {
+            const unsigned bp = __ballot_sync(kFull, pos >= 0);
+            const int slot = nA + __popc(bp & ((1u << lane) - 1u));
+            if (pos >= 0 && slot < kAPcap) AP[slot] = (uint32_t)pos;   // caller ignores AP if nA > kAPcap
+            nA += __popc(bp);
+        }
     }
     __syncwarp();
+    if (nap) *nap = nA;
     return nL;
 }
 
@@ -352,12 +363,37 @@ __device__ __forceinline__ void star_run(const Dev &g, const uint8_t *lut, uint3
     }
 }
 
+// Event-free iterations j in [j0, j1) of a star chunk: no a-b edge and no b-c edge for any
+// lane, so every valid lane's set is plain and the plain masks are the chunk's validity
+// masks.  Each iteration still enumerates its 64 sets {r, a, R[j], c}: c counts it in the
+// field of code(r, R[j]), and each key lane adds its (constant) number of c's to R[j] in the
+// class of (key, code(r, R[j])).
+template <int C>
+__device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, const uint8_t *codes, StarC &s0,
+                                          StarC &s1, bool vc0, bool vc1, unsigned cntk, uint32_t col1, uint32_t col2,
+                                          uint32_t col3, int j0, int j1) {
+#pragma unroll 2
+    for (int j = j0; j < j1; j++) {
+        const uint32_t crb = codes[j] & 3u;
+        const uint32_t incA = crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u);
+        const uint32_t incB = crb == 3u ? 1u : 0u;
+        s0.pA += vc0 ? incA : 0u;
+        s0.pB += vc0 ? incB : 0u;
+        s1.pA += vc1 ? incA : 0u;
+        s1.pB += vc1 ? incB : 0u;
+        if (cntk) {
+            const uint32_t col = crb == 1u ? col1 : (crb == 2u ? col2 : col3);
+            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cntk);
+        }
+    }
+}
+
 // chunk k of the task (r, a = R[i]): c positions [max(D - 64(k+1), i+2), D - 64k), the
-// longest chunks first
+// longest chunks first.  AP[0..nap) = positions of R adjacent to a (nap < 0: unknown).
 template <int C>
 __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
-                                           uint32_t *H, int k, int lane) {
+                                           uint32_t *H, const uint32_t *AP, int nap, int k, int lane) {
     const int64_t seg = g.hbase[r];
     const int cb = D - 64 * (k + 1);
     const int p0 = cb + lane, p1 = cb + 32 + lane;
@@ -371,11 +407,39 @@ __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uin
         if (lane == q) { M0 = m0; M1 = m1; }
     }
     const uint32_t kmask = cra | ((uint32_t)(lane % 3) + 1u) << 4 | ((uint32_t)(lane / 3) & 3u) << 8;
+    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    const unsigned cntk = __popc(M0) + __popc(M1);   // key lanes: the chunk's c's with that key
+    uint32_t col1 = 0, col2 = 0, col3 = 0;
+    if (cntk) {
+        col1 = lut[kmask | 1u << 2];
+        col2 = lut[kmask | 2u << 2];
+        col3 = lut[kmask | 3u << 2];
+    }
     const int jmain = max(i + 1, min(cb, D));           // b before every c of the chunk
     const int pmax = D - 64 * k - 1;                     // last c position of the chunk
+    int ap = 0;
+    if (nap > 0)
+        while (ap < nap && (int)AP[ap] <= i) ap++;
     // 16-bit fields: flush at least every 65535 iterations
     for (int jb = i + 1; jb < jmain; jb += 65535) {
-        star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jb, min(jmain, jb + 65535));
+        const int je = min(jmain, jb + 65535);
+        if (nap < 0) {
+            star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jb, je);
+        } else {
+            int j = jb;
+            while (j < je) {
+                const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next b-c edge
+                const int eva = ap < nap ? (int)AP[ap] : je;                            // next a-b edge
+                const int stop = min(je, min((int)min(evw, 0x3fffffffu), eva));
+                star_fast<C>(g, R, codes, s0, s1, vc0, vc1, cntk, col1, col2, col3, j, stop);
+                j = stop;
+                if (j < je) {   // an event: one general iteration
+                    star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, j, j + 1);
+                    if (j == eva) ap++;
+                    j++;
+                }
+            }
+        }
         star_c_flush<C>(g, s0, lut, H);
         star_c_flush<C>(g, s1, lut, H);
     }
@@ -621,12 +685,80 @@ __device__ __forceinline__ void cross_run(const Dev &g, const uint8_t *lut, uint
     }
 }
 
+// Event-free iterations j in [j0, j1) of a cross item (no x-R[j] edge, no R[j]-c edge for any
+// lane): every valid lane's set is plain; c counts it in the field of code(r, R[j]) and the
+// key lanes add their constant count to R[j].
+template <int C, int PART>
+__device__ __forceinline__ void cross_fast(const Dev &g, const uint32_t *R, const uint8_t *codes, CrossC &s0,
+                                           CrossC &s1, bool vc0, bool vc1, unsigned cntk, uint32_t col1,
+                                           uint32_t col2, uint32_t col3, int j0, int j1) {
+#pragma unroll 2
+    for (int j = j0; j < j1; j++) {
+        const uint32_t crj = codes[j] & 3u;
+        const uint32_t incA = crj == 1u ? 1u : (crj == 2u ? 0x10000u : 0u);
+        const uint32_t incB = crj == 3u ? 1u : 0u;
+        if (PART == 1) {
+            s0.f1A += vc0 ? incA : 0u;
+            s0.f1B += vc0 ? incB : 0u;
+            s1.f1A += vc1 ? incA : 0u;
+            s1.f1B += vc1 ? incB : 0u;
+        } else {
+            s0.f2A += vc0 ? incA : 0u;
+            s0.f2B += vc0 ? incB : 0u;
+            s1.f2A += vc1 ? incA : 0u;
+            s1.f2B += vc1 ? incB : 0u;
+        }
+        if (cntk) {
+            const uint32_t col = crj == 1u ? col1 : (crj == 2u ? col2 : col3);
+            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cntk);
+        }
+    }
+}
+
+// positions [j0, j1) of one part: event-free runs in cross_fast, events in cross_run
+template <int C, int PART>
+__device__ __forceinline__ void cross_span(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
+                                           const uint8_t *codes, const uint32_t *CA, CrossC &s0, CrossC &s1,
+                                           unsigned M0, unsigned M1, uint32_t cra, const uint32_t *AP, int nap,
+                                           int j0, int j1, int lane) {
+    if (j0 >= j1) return;
+    if (nap < 0) {
+        cross_run<C, PART>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j0, j1, lane);
+        return;
+    }
+    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    const unsigned cntk = __popc(M0) + __popc(M1);
+    const uint32_t kc = (uint32_t)lane + 1u;
+    uint32_t col1 = 0, col2 = 0, col3 = 0;
+    if (cntk) {
+        col1 = PART == 1 ? lut[cra | 1u << 2 | kc << 8] : lut[1u | cra << 2 | kc << 10];
+        col2 = PART == 1 ? lut[cra | 2u << 2 | kc << 8] : lut[2u | cra << 2 | kc << 10];
+        col3 = PART == 1 ? lut[cra | 3u << 2 | kc << 8] : lut[3u | cra << 2 | kc << 10];
+    }
+    int ap = 0;
+    while (ap < nap && (int)AP[ap] < j0) ap++;
+    int j = j0;
+    while (j < j1) {
+        const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next R[j]-c edge
+        const int eva = ap < nap ? (int)AP[ap] : j1;                            // next x-R[j] edge
+        const int stop = min(j1, min((int)min(evw, 0x3fffffffu), eva));
+        cross_fast<C, PART>(g, R, codes, s0, s1, vc0, vc1, cntk, col1, col2, col3, j, stop);
+        j = stop;
+        if (j < j1) {
+            cross_run<C, PART>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j, j + 1, lane);
+            if (j == eva) ap++;
+            j++;
+        }
+    }
+}
+
 // item (k, jb): c = L_x[64k .. 64k+63], positions j in block jb of length kCrossBlock
 template <int C>
 __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint8_t *codes, const uint32_t *La, int nL,
                                            const uint32_t *CAbeg, const uint32_t *CAlen, const uint32_t *CA,
-                                           uint32_t cra, uint32_t a, uint32_t *H, int k, int jb, int lane) {
+                                           uint32_t cra, uint32_t a, uint32_t *H, const uint32_t *AP, int nap, int k,
+                                           int jb, int lane) {
     const int j0 = jb * kCrossBlock, j1 = min(D, j0 + kCrossBlock);
     CrossC s0, s1;
     cross_c_init(s0, La, nL, CAbeg, CAlen, CA, 64 * k + lane, j0);
@@ -637,8 +769,12 @@ __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uin
         const unsigned m0 = __ballot_sync(kFull, s0.key == q), m1 = __ballot_sync(kFull, s1.key == q);
         if (lane == q) { M0 = m0; M1 = m1; }
     }
-    cross_run<C, 2>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j0, min(j1, i), lane);
-    cross_run<C, 1>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, max(j0, i + 1), j1, lane);
+    cross_span<C, 2>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, AP, nap, j0, min(j1, i), lane);
+    if (min(j1, i) > j0 && i + 1 < j1) {   // j = i is a's own position: skip the pointers past it
+        while (s0.npos <= (uint32_t)i) { s0.q++; cross_c_next(CA, s0); }
+        while (s1.npos <= (uint32_t)i) { s1.q++; cross_c_next(CA, s1); }
+    }
+    cross_span<C, 1>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, AP, nap, max(j0, i + 1), j1, lane);
     cross_c_flush<C>(g, s0, lut, H, cra);
     cross_c_flush<C>(g, s1, lut, H, cra);
     if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
@@ -705,7 +841,8 @@ template <int K, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
-                                           int *s_ca, const Staged *st, int w, int lane) {
+                                           int *s_ca, const Staged *st, const uint32_t *AP, int nap, int w,
+                                           int lane) {
     constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
@@ -755,13 +892,13 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
             if (it < nch) {
-                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, it, lane);
+                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, AP, nap, it, lane);
             } else if (it < nch + nB) {
                 const int b_it = it - nch;
                 if (g.skip & 2) continue;
                 if (cross)
-                    cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, b_it / njb,
-                                  b_it % njb, lane);
+                    cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, AP, nap,
+                                  b_it / njb, b_it % njb, lane);
                 else
                     item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
                                        glist(g, R[i + 1 + b_it] >> 2), lane);
@@ -782,7 +919,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item;
-    __shared__ int s_nL, s_work, s_ca;
+    __shared__ int s_nL, s_work, s_ca, s_nap;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
@@ -794,6 +931,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         uint32_t *hb = HSMEM ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
         uint32_t *R = hb + L.R, *La = hb + L.La, *Ba = hb + L.Ba;
         uint32_t *Bl = hb + L.Bl + wid * L.lw;
+        uint32_t *AP = hb + L.AP;   // positions of R adjacent to a (kAPcap)
         uint8_t *codes = reinterpret_cast<uint8_t *>(hb + L.Bb);   // heavy: per-task code bytes
         if (!HSMEM) {   // zero this CTA's global bitmaps once
             for (int q = tid; q < L.Bl + kWarps * L.lw - L.Ba; q += kBlock) hb[L.Ba + q] = 0;
@@ -818,8 +956,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
             }
             if (wid == 0) {
-                const int nL = build_a(g, r, glist(g, R[i] >> 2), R, D, Ba, La, lane);
+                int nap = 0;
+                const int nL = build_a(g, r, glist(g, R[i] >> 2), R, D, Ba, La, lane, AP, &nap);
                 if (lane == 0) {
+                    s_nap = nap;
                     s_nL = nL;
                     s_work = 0;
                     s_ca = 0;
@@ -832,7 +972,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
             }
             task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, nullptr, wid, lane);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, nullptr, AP,
+                                  s_nap <= kAPcap ? s_nap : -1, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -879,7 +1020,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 const int nL = build_a(g, r, al, R, D, Ba, La, lane);
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kLcap, lane);
                 task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
-                                 0, lane);
+                                 nullptr, -1, 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
@@ -1009,7 +1150,8 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
     L.Ba = L.La + md;
     L.Bb = L.Ba + L.bw;                  // heavy: the per-task code bytes (md bytes)
     L.Bl = L.Bb + (md + 3) / 4;
-    const int heavy_words = L.Bl + kWarps * L.lw;
+    L.AP = L.Bl + kWarps * L.lw;
+    const int heavy_words = L.AP + kAPcap;
     const int light_words = kWarps * kLightWords;
     const int hist_words = kWarps * C;
     const int budget_words = (104 * 1024) / 4 - hist_words;   // keep 2 CTAs per SM
