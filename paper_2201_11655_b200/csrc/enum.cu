@@ -64,6 +64,7 @@ struct Dev {
     int heavy_in_smem;                        // heavy buffers fit in shared memory
     int big;                                  // degrees so large a task could overflow u32 histograms
     int maxdeg;
+    int off32;                                // n * C < 2^32: 32-bit accumulator offsets
     int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop
     uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
     int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
@@ -368,23 +369,51 @@ __device__ __forceinline__ void star_run(const Dev &g, const uint8_t *lut, uint3
 // masks.  Each iteration still enumerates its 64 sets {r, a, R[j], c}: c counts it in the
 // field of code(r, R[j]), and each key lane adds its (constant) number of c's to R[j] in the
 // class of (key, code(r, R[j])).
-template <int C>
-__device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, const uint8_t *codes, StarC &s0,
-                                          StarC &s1, bool vc0, bool vc1, unsigned cntk, uint32_t col1, uint32_t col2,
-                                          uint32_t col3, int j0, int j1) {
-#pragma unroll 2
+// row offset of vertex v's column col in the accumulator (32-bit when n*C < 2^32)
+template <int C, bool OFF32>
+__device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, uint32_t col) {
+    if (OFF32) return g.acc + (v * (uint32_t)C + col);
+    return g.acc + ((size_t)v * C + col);
+}
+
+template <int C, bool FULL, bool OFF32>
+__device__ __forceinline__ void star_fast_t(const Dev &g, const uint32_t *R, StarC &s0, StarC &s1, bool vc0,
+                                            bool vc1, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
+                                            int j0, int j1) {
+#pragma unroll 4
     for (int j = j0; j < j1; j++) {
-        const uint32_t crb = codes[j] & 3u;
+        const uint32_t e = R[j];   // rank(b) << 2 | code(r, b)
+        const uint32_t crb = e & 3u;
         const uint32_t incA = crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u);
         const uint32_t incB = crb == 3u ? 1u : 0u;
-        s0.pA += vc0 ? incA : 0u;
-        s0.pB += vc0 ? incB : 0u;
-        s1.pA += vc1 ? incA : 0u;
-        s1.pB += vc1 ? incB : 0u;
+        if (FULL) {
+            s0.pA += incA;
+            s0.pB += incB;
+            s1.pA += incA;
+            s1.pB += incB;
+        } else {
+            s0.pA += vc0 ? incA : 0u;
+            s0.pB += vc0 ? incB : 0u;
+            s1.pA += vc1 ? incA : 0u;
+            s1.pB += vc1 ? incB : 0u;
+        }
         if (cntk) {
             const uint32_t col = crb == 1u ? col1 : (crb == 2u ? col2 : col3);
-            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cntk);
+            atomicAdd(acc_at<C, OFF32>(g, e >> 2, col), (unsigned long long)cntk);
         }
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarC &s0, StarC &s1, bool vc0, bool vc1,
+                                          bool full, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
+                                          int j0, int j1) {
+    if (j0 >= j1) return;
+    if (g.off32) {
+        if (full) star_fast_t<C, true, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
+        else star_fast_t<C, false, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
+    } else {
+        star_fast_t<C, false, false>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
     }
 }
 
@@ -408,6 +437,7 @@ __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uin
     }
     const uint32_t kmask = cra | ((uint32_t)(lane % 3) + 1u) << 4 | ((uint32_t)(lane / 3) & 3u) << 8;
     const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    const bool full = __all_sync(kFull, vc0 && vc1);
     const unsigned cntk = __popc(M0) + __popc(M1);   // key lanes: the chunk's c's with that key
     uint32_t col1 = 0, col2 = 0, col3 = 0;
     if (cntk) {
@@ -431,7 +461,7 @@ __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uin
                 const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next b-c edge
                 const int eva = ap < nap ? (int)AP[ap] : je;                            // next a-b edge
                 const int stop = min(je, min((int)min(evw, 0x3fffffffu), eva));
-                star_fast<C>(g, R, codes, s0, s1, vc0, vc1, cntk, col1, col2, col3, j, stop);
+                star_fast<C>(g, R, s0, s1, vc0, vc1, full, cntk, col1, col2, col3, j, stop);
                 j = stop;
                 if (j < je) {   // an event: one general iteration
                     star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, j, j + 1);
@@ -688,30 +718,46 @@ __device__ __forceinline__ void cross_run(const Dev &g, const uint8_t *lut, uint
 // Event-free iterations j in [j0, j1) of a cross item (no x-R[j] edge, no R[j]-c edge for any
 // lane): every valid lane's set is plain; c counts it in the field of code(r, R[j]) and the
 // key lanes add their constant count to R[j].
-template <int C, int PART>
-__device__ __forceinline__ void cross_fast(const Dev &g, const uint32_t *R, const uint8_t *codes, CrossC &s0,
-                                           CrossC &s1, bool vc0, bool vc1, unsigned cntk, uint32_t col1,
-                                           uint32_t col2, uint32_t col3, int j0, int j1) {
-#pragma unroll 2
+template <int C, int PART, bool FULL, bool OFF32>
+__device__ __forceinline__ void cross_fast_t(const Dev &g, const uint32_t *R, CrossC &s0, CrossC &s1, bool vc0,
+                                             bool vc1, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
+                                             int j0, int j1) {
+#pragma unroll 4
     for (int j = j0; j < j1; j++) {
-        const uint32_t crj = codes[j] & 3u;
+        const uint32_t e = R[j];   // rank(R[j]) << 2 | code(r, R[j])
+        const uint32_t crj = e & 3u;
         const uint32_t incA = crj == 1u ? 1u : (crj == 2u ? 0x10000u : 0u);
         const uint32_t incB = crj == 3u ? 1u : 0u;
-        if (PART == 1) {
-            s0.f1A += vc0 ? incA : 0u;
-            s0.f1B += vc0 ? incB : 0u;
-            s1.f1A += vc1 ? incA : 0u;
-            s1.f1B += vc1 ? incB : 0u;
+        uint32_t &a0 = PART == 1 ? s0.f1A : s0.f2A, &b0 = PART == 1 ? s0.f1B : s0.f2B;
+        uint32_t &a1 = PART == 1 ? s1.f1A : s1.f2A, &b1 = PART == 1 ? s1.f1B : s1.f2B;
+        if (FULL) {
+            a0 += incA;
+            b0 += incB;
+            a1 += incA;
+            b1 += incB;
         } else {
-            s0.f2A += vc0 ? incA : 0u;
-            s0.f2B += vc0 ? incB : 0u;
-            s1.f2A += vc1 ? incA : 0u;
-            s1.f2B += vc1 ? incB : 0u;
+            a0 += vc0 ? incA : 0u;
+            b0 += vc0 ? incB : 0u;
+            a1 += vc1 ? incA : 0u;
+            b1 += vc1 ? incB : 0u;
         }
         if (cntk) {
             const uint32_t col = crj == 1u ? col1 : (crj == 2u ? col2 : col3);
-            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cntk);
+            atomicAdd(acc_at<C, OFF32>(g, e >> 2, col), (unsigned long long)cntk);
         }
+    }
+}
+
+template <int C, int PART>
+__device__ __forceinline__ void cross_fast(const Dev &g, const uint32_t *R, CrossC &s0, CrossC &s1, bool vc0,
+                                           bool vc1, bool full, unsigned cntk, uint32_t col1, uint32_t col2,
+                                           uint32_t col3, int j0, int j1) {
+    if (j0 >= j1) return;
+    if (g.off32) {
+        if (full) cross_fast_t<C, PART, true, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
+        else cross_fast_t<C, PART, false, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
+    } else {
+        cross_fast_t<C, PART, false, false>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
     }
 }
 
@@ -727,6 +773,7 @@ __device__ __forceinline__ void cross_span(const Dev &g, const uint8_t *lut, uin
         return;
     }
     const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
+    const bool full = __all_sync(kFull, vc0 && vc1);
     const unsigned cntk = __popc(M0) + __popc(M1);
     const uint32_t kc = (uint32_t)lane + 1u;
     uint32_t col1 = 0, col2 = 0, col3 = 0;
@@ -742,7 +789,7 @@ __device__ __forceinline__ void cross_span(const Dev &g, const uint8_t *lut, uin
         const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next R[j]-c edge
         const int eva = ap < nap ? (int)AP[ap] : j1;                            // next x-R[j] edge
         const int stop = min(j1, min((int)min(evw, 0x3fffffffu), eva));
-        cross_fast<C, PART>(g, R, codes, s0, s1, vc0, vc1, cntk, col1, col2, col3, j, stop);
+        cross_fast<C, PART>(g, R, s0, s1, vc0, vc1, full, cntk, col1, col2, col3, j, stop);
         j = stop;
         if (j < j1) {
             cross_run<C, PART>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j, j + 1, lane);
@@ -1385,6 +1432,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.heavy_in_smem = heavy_in_smem ? 1 : 0;
     d.big = g->max_degree > 32767 ? 1 : 0;
     d.maxdeg = (int)g->max_degree;
+    d.off32 = (uint64_t)std::max<int64_t>(g->n, 1) * C < (1ull << 32) ? 1 : 0;
     d.hbase = g->hbase;
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
