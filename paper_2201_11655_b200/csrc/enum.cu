@@ -601,7 +601,7 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
 // c's code(x, c) and the iteration's code(r, R[j]): c and the pair (r, x) accumulate per-lane
 // 16-bit counters, R[j] gets popc(plain & M_k) per key k = code(x, c) from lanes 0..2, and
 // the remaining sets are classified one by one (cross_slow).
-constexpr int kCrossBlock = 2048;   // j-block length (< 2^16: the per-lane 16-bit counters)
+constexpr int kCrossBlock = 1024;   // j-block length (< 2^16: the per-lane 16-bit counters)
 
 struct CrossC {
     uint32_t c, cxc, npos, ncode, q, q1;
@@ -933,15 +933,21 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         const int nck = (nL + 63) / 64, njb = (D + kCrossBlock - 1) / kCrossBlock;
         const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
         const int total = nch + nB + nL;
+        // longest first across kinds: star chunks longer than a cross block, the "2+1" items,
+        // the remaining star chunks, then the b-in-L_a items
+        const int nlong = cross ? max(0, min(nch, (D - i - 2 - kCrossBlock) / 64 + 1)) : nch;
         for (;;) {
             int it = 0;
             if (lane == 0) it = atomicAdd(wctr, 1);
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
-            if (it < nch) {
-                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, AP, nap, it, lane);
-            } else if (it < nch + nB) {
-                const int b_it = it - nch;
+            int star_k = -1, b_it = -1;
+            if (it < nlong) star_k = it;
+            else if (it < nlong + nB) b_it = it - nlong;
+            else if (it < nch + nB) star_k = it - nB;
+            if (star_k >= 0) {
+                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, AP, nap, star_k, lane);
+            } else if (b_it >= 0) {
                 if (g.skip & 2) continue;
                 if (cross)
                     cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, AP, nap,
