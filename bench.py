@@ -35,6 +35,11 @@ import graphgen as G  # noqa: E402
 METRIC = "4-motif per-vertex counting: motifs/sec and edges/sec at 1/2/4/8 B200"
 BYTES_PER_MOTIF = {3: 36, 4: 52}   # 4 B neighbour entry + (k-1) x 16 B u64 RMW
 FALLBACK_HBM = 6650.0             # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
+# Which resource bounds k_enum, by graph family (ncu, profiles/r01_*): on the power-law graphs the
+# hub-leaf counter rows stay in L2 (DRAM at ~13% of peak) and the kernel is integer-issue bound;
+# on Erdos-Renyi the per-set counter updates scatter over a matrix >> L2 and HBM sectors bound it.
+BOUND = {"ba": "alu", "gnp": "hbm"}
+LANES_PER_SM = 128                # 4 SMSPs x 32 lanes: one integer op per lane per clock (issue limit)
 
 
 def parse():
@@ -58,6 +63,16 @@ def peak_hbm():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def peak_alu(nsm):
+    """Integer issue peak, int-op/s: SMs x 128 lanes x max SM clock (MEASURED_PEAKS.json sm_max_mhz)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz, src = float(json.load(f)["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
+    except Exception:
+        mhz, src = 1965.0, "B200 max SM clock 1965 MHz (fallback)"
+    return nsm * LANES_PER_SM * mhz * 1e6, f"{nsm} SMs x {LANES_PER_SM} int lanes x {mhz:.0f} MHz ({src})"
 
 
 def ncu_traffic(config, k):
@@ -240,7 +255,7 @@ def main():
     torch.cuda.synchronize()
     clocks = Clocks(local) if rank == 0 else None
     launches0 = vdmc.kernel_launches()
-    step_ms, enum_ms = [], []
+    step_ms, enum_ms, phase_ms = [], [], []
     for _ in range(args.steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -250,7 +265,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        enum_ms.append(g.timings()["enum"])
+        tm = g.timings()
+        enum_ms.append(tm["enum"])
+        phase_ms.append(tm)
         g.close()
         del out
     launches = vdmc.kernel_launches() - launches0
@@ -301,11 +318,27 @@ def main():
         value = total_sets / (ms_per_step / 1e3)
         peak, peak_src = peak_hbm()
         enum_avg = statistics.mean(enum_ms)
-        # roofline of the dominant kernel (the enumeration): algorithmic bytes per launch =
-        # motifs this rank enumerates x B_k; per-rank share approximated by 1/world
-        alg_bytes = total_sets / world * BYTES_PER_MOTIF[k]
-        achieved = alg_bytes / (enum_avg / 1e3) / 1e9
+        # roofline of the dominant kernel (the enumeration), per launch; this rank's share of the
+        # motifs approximated by 1/world.  hbm: algorithmic bytes = motifs x B_k.
+        # alu: algorithmic integer ops = motifs x k, the k member increments of P:118.
         traffic = ncu_traffic(args.config, k)
+        motifs_launch = total_sets / world
+        bound = BOUND[G.CONFIGS[args.config]["kind"]]
+        if bound == "hbm":
+            achieved = motifs_launch * BYTES_PER_MOTIF[k] / (enum_avg / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic": f"{BYTES_PER_MOTIF[k]} B per motif (SURVEY 8(d) M3) x {motifs_launch:.4g} motifs"}
+        else:
+            palu, palu_src = peak_alu(torch.cuda.get_device_properties(dev).multi_processor_count)
+            achieved = motifs_launch * k / (enum_avg / 1e3) / 1e12
+            roof = {"bound": "alu", "achieved": achieved, "peak": palu / 1e12, "unit": "Tint-op/s",
+                    "frac": achieved * 1e12 / palu, "traffic": traffic, "peak_source": palu_src,
+                    "algorithmic": f"{k} counter increments per motif (P:118) x {motifs_launch:.4g} motifs",
+                    "hbm_achieved_model_GBs": motifs_launch * BYTES_PER_MOTIF[k] / (enum_avg / 1e3) / 1e9}
+        roof["kernel"] = f"k_enum<{k}>"
+        if traffic:
+            roof["traffic_GBs"] = traffic / (enum_avg / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "motifs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -316,10 +349,10 @@ def main():
                        "arcs": arcs, "parallelism": f"dp{world} (graph replicated, task slices, NCCL reduce)"
                        if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write); count matrix >> L2"},
-            "kernel_ms": {"enum_avg": enum_avg, "step_avg": ms_per_step, "enum_share": enum_avg / ms_per_step},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_motif": BYTES_PER_MOTIF[k], "kernel": f"k_enum<{k}>"},
+            "kernel_ms": {"enum_avg": enum_avg, "step_avg": ms_per_step, "enum_share": enum_avg / ms_per_step,
+                          **{f"{key}_avg": statistics.mean(t[key] for t in phase_ms)
+                             for key in ("build", "plan", "finalize")}},
+            "roofline": roof,
             "e2e": {"value": total_sets / (E_ms / 1e3), "unit": "motifs/s",
                     "h2d_bytes_per_step": int(2 * 4 * arcs),
                     "d2h_bytes_per_step": int(n * C * 8), "ms_per_step": E_ms},

@@ -2,6 +2,8 @@
 // error reporting, and the motif-class lookup table.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstring>
 #include <mutex>
@@ -27,6 +29,15 @@ vdmc_status fail(vdmc_status st, const char *fmt, ...) {
 }
 
 void count_launch(int n) { g_launches += n; }
+
+void trace(const char *what) {
+    static const bool on = [] { const char *e = getenv("VDMC_TRACE"); return e && e[0] == '1'; }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[vdmc trace] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
 
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s) {
     static std::mutex mu;

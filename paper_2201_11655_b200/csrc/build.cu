@@ -153,6 +153,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     VDMC_CUDA(cudaEventCreate(&e0));
     VDMC_CUDA(cudaEventCreate(&e1));
     VDMC_CUDA(cudaEventRecord(e0, s));
+    trace("build start");
     g->n = n;
     Tmp tmp(s);
     const int vb = bits_for(std::max<int64_t>(n, 2));
@@ -174,6 +175,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     VDMC_CUDA(cudaMemsetAsync(flags + 1, 0, 3 * sizeof(unsigned long long), s));
     VDMC_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
     VDMC_CUDA(cudaMemsetAsync(deg_r, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    trace("build allocs+memsets");
 
     // ---- S1: entries, sort, OR-merge
     if (m > 0) {
@@ -185,6 +187,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)L, 0, 34 + vb, s));
         VDMC_CUDA(tmp.alloc((char **)&tstore, tb));
         VDMC_CUDA(cub::DeviceRadixSort::SortKeys(tstore, tb, db, (int)L, 0, 34 + vb, s));
+        trace("sort1 enqueued");
         count_launch(2 * ((34 + vb + 7) / 8));
         uint64_t *sorted = db.Current();
         k_heads<<<grid_for(L), kThreads, 0, s>>>(L, sorted, head);
@@ -207,6 +210,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         VDMC_CUDA(cudaMemcpyAsync(&last_head, head + L - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaMemcpyAsync(hf, flags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
+        trace("sync after merge");
         if (hf[0] != ~0ull) {
             long long e = (long long)(hf[0] >> 2);
             if ((hf[0] & 3) == 1) return fail(VDMC_ESELFLOOP, "arc %lld is a self-loop", e);
@@ -242,6 +246,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         }
     }
 
+    trace("order");
     // ---- S2: relabel + sort + CSR
     VDMC_CUDA(dalloc((void **)&g->off, sizeof(int64_t) * (n + 1), s));
     VDMC_CUDA(dalloc((void **)&g->split, sizeof(int64_t) * std::max<int64_t>(n, 1), s));
@@ -261,6 +266,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         VDMC_CUDA(cub::DeviceRadixSort::SortKeys(ts, tb, db, (int)nnz, 0, 34 + vb, s));
         count_launch(2 * ((34 + vb + 7) / 8));
         k_adj<<<grid_for(nnz), kThreads, 0, s>>>(nnz, db.Current(), g->adj);
+        trace("sort2 enqueued");
         VDMC_LAUNCH();
     }
     if (n > 0) {
@@ -291,6 +297,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         VDMC_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
         g->max_degree = hmax;
+        trace("sync max degree");
     }
     g->ntasks = nnz / 2;
     VDMC_CUDA(dalloc((void **)&g->task_root, sizeof(int32_t) * std::max<int64_t>(g->ntasks, 1), s));
@@ -301,6 +308,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     VDMC_CUDA(cudaEventRecord(e1, s));
     VDMC_CUDA(cudaStreamSynchronize(s));
     VDMC_CUDA(cudaEventElapsedTime(&g->build_ms, e0, e1));
+    trace("build end sync");
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return VDMC_OK;

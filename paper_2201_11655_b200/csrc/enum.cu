@@ -1383,6 +1383,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
     vdmc_status st = ensure_roots(g, s);
     if (st) return st;
+    trace("ensure_roots");
     bool heavy_in_smem = true;
     int64_t per_cta = 0;
     // VDMC_HEAVY_GLOBAL=1 forces the global-memory fallback for heavy-task buffers (tests)
@@ -1409,6 +1410,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     VDMC_CUDA(cudaMemsetAsync(g->acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
     VDMC_CUDA(cudaMemsetAsync(g->ctr, 0, 2 * sizeof(unsigned long long), s));
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[1], s));
+    trace("scratch+memset");
     Dev d{};
     d.off = g->off;
     d.split = g->split;
@@ -1455,12 +1457,15 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
         VDMC_LAUNCH();
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[3], s));
+    trace("enum+finalize enqueued");
     return VDMC_OK;
 }
 
 vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi, cudaStream_t s) {
+    trace("count start");
     vdmc_status st = ensure_acc(g, k, s);
     if (st) return st;
+    trace("ensure_acc");
     return k == 3 ? run<3>(g, counts, lo, hi, s) : run<4>(g, counts, lo, hi, s);
 }
 

@@ -19,6 +19,8 @@ void count_launch(int n = 1);
 // paying cudaMalloc/cudaFree (page mapping of GB-sized count matrices) every call.
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s);
 void dfree(void *p, cudaStream_t s);
+// Host-side trace (VDMC_TRACE=1): prints the host milliseconds since the previous point.
+void trace(const char *what);
 
 #define VDMC_CUDA(call)                                                                  \
     do {                                                                                 \
