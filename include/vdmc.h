@@ -128,8 +128,14 @@ vdmc_status vdmc_last_timings(const vdmc_graph *g, float *ms, int nms);
 /* Number of kernels this library has launched in this process (all graphs, all devices). */
 int64_t vdmc_kernel_launches(void);
 
-/* Free the graph and its device memory (NULL is a no-op). */
+/* Free the graph and its device memory (NULL is a no-op).  Large device buffers (>= 4 MiB)
+ * return to the library's process-wide block cache, so the next build / count on this device
+ * reuses them without page mapping; vdmc_trim releases the idle ones. */
 void vdmc_free_graph(vdmc_graph *g);
+
+/* Synchronise `device` and release the library's idle cached device blocks to the driver.
+ * Blocks held by live graphs are untouched.  Errors: VDMC_ENODEV (no such device), VDMC_ECUDA. */
+vdmc_status vdmc_trim(int device);
 
 /* Thread-local message for the last failing call on this thread ("" if none). */
 const char *vdmc_last_error(void);

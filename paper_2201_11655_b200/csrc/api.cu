@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "vdmc_internal.cuh"
@@ -39,27 +40,113 @@ void trace(const char *what) {
     last = now;
 }
 
+// Device memory.  Small buffers: stream-ordered allocations from the device's default pool
+// (release threshold = max, so freed memory stays mapped).  Buffers >= kBigBytes (count
+// matrices, sort keys, scratch): a process-wide cache of cudaMalloc'd blocks, reused best-fit
+// across calls and graphs, so a step never pays page mapping for GB-sized buffers and the pool
+// never fragments them.  A cached block remembers the stream it was freed on and an event
+// recorded there; a reuse on another stream waits for that event (stream-ordered semantics).
+namespace {
+constexpr size_t kBigBytes = size_t(4) << 20;
+constexpr size_t kGrain = size_t(2) << 20;
+struct Block {
+    void *p = nullptr;
+    size_t bytes = 0;
+    int dev = 0;
+    cudaStream_t last = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+std::mutex g_mem_mu;
+std::vector<Block> g_free;                  // cached, idle
+std::unordered_map<void *, Block> g_live;   // handed out
+bool g_pool_configured[64] = {};
+}  // namespace
+
+static cudaError_t configure_pool(int dev) {
+    if (dev >= 64 || g_pool_configured[dev]) return cudaSuccess;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = ~0ull;
+    if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
+    g_pool_configured[dev] = true;
+    return cudaSuccess;
+}
+
+// free every idle cached block of `dev` (caller holds g_mem_mu)
+static void trim_locked(int dev) {
+    for (size_t i = 0; i < g_free.size();) {
+        if (g_free[i].dev == dev) {
+            cudaEventSynchronize(g_free[i].ready);
+            cudaFree(g_free[i].p);
+            cudaEventDestroy(g_free[i].ready);
+            g_free[i] = g_free.back();
+            g_free.pop_back();
+        } else {
+            i++;
+        }
+    }
+}
+
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s) {
-    static std::mutex mu;
-    static bool configured[64] = {};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (dev < 64 && !configured[dev]) {
-            cudaMemPool_t pool;
-            if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
-            uint64_t thr = ~0ull;
-            if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
-            configured[dev] = true;
-        }
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    if ((e = configure_pool(dev)) != cudaSuccess) return e;
+    if (bytes < kBigBytes) return cudaMallocAsync(p, bytes ? bytes : 1, s);
+    const size_t need = (bytes + kGrain - 1) / kGrain * kGrain;
+    int best = -1;
+    for (size_t i = 0; i < g_free.size(); i++) {   // best fit within 25% + one grain
+        const Block &b = g_free[i];
+        if (b.dev == dev && b.bytes >= need && b.bytes <= need + need / 4 + kGrain &&
+            (best < 0 || b.bytes < g_free[best].bytes))
+            best = (int)i;
     }
-    return cudaMallocAsync(p, bytes ? bytes : 1, s);
+    Block b;
+    if (best >= 0) {
+        b = g_free[best];
+        g_free[best] = g_free.back();
+        g_free.pop_back();
+        if (b.last != s && (e = cudaStreamWaitEvent(s, b.ready, 0)) != cudaSuccess) return e;
+    } else {
+        e = cudaMalloc(&b.p, need);
+        if (e == cudaErrorMemoryAllocation) {   // give the idle cache back and retry once
+            cudaGetLastError();
+            trim_locked(dev);
+            e = cudaMalloc(&b.p, need);
+        }
+        if (e != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&b.ready, cudaEventDisableTiming)) != cudaSuccess) {
+            cudaFree(b.p);
+            return e;
+        }
+        b.bytes = need;
+        b.dev = dev;
+    }
+    g_live[b.p] = b;
+    *p = b.p;
+    return cudaSuccess;
 }
 
 void dfree(void *p, cudaStream_t s) {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    auto it = g_live.find(p);
+    if (it == g_live.end()) {
+        cudaFreeAsync(p, s);
+        return;
+    }
+    Block b = it->second;
+    g_live.erase(it);
+    b.last = s;
+    cudaEventRecord(b.ready, s);
+    g_free.push_back(b);
+}
+
+void trim_cache(int dev) {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    trim_locked(dev);
 }
 
 // ------------------------------------------------------------ class table
@@ -210,7 +297,7 @@ vdmc_status vdmc_build_graph_edges(int64_t n, int64_t m, const int32_t *src, con
     const int32_t *d_src = src, *d_dst = dst;
     int32_t *tmp = nullptr;
     if (!on_device && m > 0) {
-        cudaError_t e1 = cudaMallocAsync((void **)&tmp, sizeof(int32_t) * 2 * m, s);
+        cudaError_t e1 = dalloc((void **)&tmp, sizeof(int32_t) * 2 * m, s);
         if (e1 != cudaSuccess) { delete g; return fail(VDMC_ENOMEM, "cudaMallocAsync: %s", cudaGetErrorString(e1)); }
         cudaMemcpyAsync(tmp, src, sizeof(int32_t) * m, cudaMemcpyHostToDevice, s);
         cudaMemcpyAsync(tmp + m, dst, sizeof(int32_t) * m, cudaMemcpyHostToDevice, s);
@@ -218,7 +305,7 @@ vdmc_status vdmc_build_graph_edges(int64_t n, int64_t m, const int32_t *src, con
         d_dst = tmp + m;
     }
     st = build_device(n, m, d_src, d_dst, rank, device, s, g);
-    if (tmp) cudaFreeAsync(tmp, s);
+    if (tmp) dfree(tmp, s);
     if (st) { vdmc_free_graph(g); return st; }
     *out = g;
     return VDMC_OK;
@@ -356,6 +443,15 @@ vdmc_status vdmc_last_timings(const vdmc_graph *g, float *ms, int nms) {
     }
     gg->last_ms[0] = g->build_ms;
     for (int i = 0; i < nms; i++) ms[i] = g->last_ms[i];
+    return VDMC_OK;
+}
+
+vdmc_status vdmc_trim(int device) {
+    vdmc_status st = check_device(device);
+    if (st) return st;
+    VDMC_CUDA(cudaSetDevice(device));
+    VDMC_CUDA(cudaDeviceSynchronize());
+    trim_cache(device);
     return VDMC_OK;
 }
 

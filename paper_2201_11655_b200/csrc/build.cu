@@ -131,9 +131,9 @@ struct Tmp {   // stream-ordered temporaries, freed on scope exit
     cudaStream_t s;
     std::vector<void *> ptrs;
     explicit Tmp(cudaStream_t st) : s(st) {}
-    ~Tmp() { for (void *p : ptrs) cudaFreeAsync(p, s); }
+    ~Tmp() { for (void *p : ptrs) dfree(p, s); }
     template <class T> cudaError_t alloc(T **p, size_t count) {
-        cudaError_t e = cudaMallocAsync((void **)p, std::max<size_t>(1, count) * sizeof(T), s);
+        cudaError_t e = dalloc((void **)p, std::max<size_t>(1, count) * sizeof(T), s);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }

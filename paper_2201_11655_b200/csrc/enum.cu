@@ -1247,10 +1247,10 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
     const int64_t n = g->n, T = g->ntasks;
     char *fh = nullptr, *fl = nullptr, *ft = nullptr;
     int64_t *nsel = nullptr;
-    VDMC_CUDA(cudaMallocAsync(&fh, std::max<int64_t>(n, 1), s));
-    VDMC_CUDA(cudaMallocAsync(&fl, std::max<int64_t>(n, 1), s));
-    VDMC_CUDA(cudaMallocAsync(&ft, std::max<int64_t>(T, 1), s));
-    VDMC_CUDA(cudaMallocAsync(&nsel, sizeof(int64_t) * 2, s));
+    VDMC_CUDA(dalloc((void **)&fh, std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(dalloc((void **)&fl, std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(dalloc((void **)&ft, std::max<int64_t>(T, 1), s));
+    VDMC_CUDA(dalloc((void **)&nsel, sizeof(int64_t) * 2, s));
     if (!g->light_root) VDMC_CUDA(dalloc((void **)&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
     if (!g->heavy_task) VDMC_CUDA(dalloc((void **)&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1), s));
     int64_t hn[2] = {0, 0};
@@ -1264,12 +1264,12 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
         void *ts = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&ts, std::max(tb, tb2), s));
+        VDMC_CUDA(dalloc((void **)&ts, std::max(tb, tb2), s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
         count_launch(2);
         VDMC_CUDA(cudaMemcpyAsync(hn, nsel, sizeof hn, cudaMemcpyDeviceToHost, s));
-        cudaFreeAsync(ts, s);
+        dfree(ts, s);
     }
     // heavy roots (rank order) and the induced adjacency of each one's N+(r)
     int64_t nhr = 0;
@@ -1280,25 +1280,25 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         size_t tb = 0;
         VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, fh, g->hroots, nsel, (int)n, s));
         void *ts = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&ts, tb, s));
+        VDMC_CUDA(dalloc((void **)&ts, tb, s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, fh, g->hroots, nsel, (int)n, s));
         count_launch(1);
         VDMC_CUDA(cudaMemcpyAsync(&nhr, nsel, sizeof nhr, cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
-        cudaFreeAsync(ts, s);
+        dfree(ts, s);
     }
     g->nhroots = nhr;
     if (nhr > 0) {
         int64_t *dlist = nullptr, *segs = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&dlist, sizeof(int64_t) * (nhr + 1), s));
-        VDMC_CUDA(cudaMallocAsync(&segs, sizeof(int64_t) * (nhr + 1), s));
+        VDMC_CUDA(dalloc((void **)&dlist, sizeof(int64_t) * (nhr + 1), s));
+        VDMC_CUDA(dalloc((void **)&segs, sizeof(int64_t) * (nhr + 1), s));
         VDMC_CUDA(cudaMemsetAsync(dlist + nhr, 0, sizeof(int64_t), s));
         k_heavy_d<<<148 * 4, 256, 0, s>>>(nhr, g->hroots, g->off, g->split, dlist);
         VDMC_LAUNCH();
         size_t tb = 0;
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, dlist, segs, (int)(nhr + 1), s));
         void *ts = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&ts, tb, s));
+        VDMC_CUDA(dalloc((void **)&ts, tb, s));
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts, tb, dlist, segs, (int)(nhr + 1), s));
         count_launch(2);
         k_scatter_hbase<<<148 * 4, 256, 0, s>>>(nhr, g->hroots, segs, g->hbase);
@@ -1306,10 +1306,10 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         int64_t sumD = 0;
         VDMC_CUDA(cudaMemcpyAsync(&sumD, segs + nhr, sizeof sumD, cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
-        cudaFreeAsync(ts, s);
+        dfree(ts, s);
         // counts -> offsets -> entries
         int64_t *cnt = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&cnt, sizeof(int64_t) * (sumD + 1), s));
+        VDMC_CUDA(dalloc((void **)&cnt, sizeof(int64_t) * (sumD + 1), s));
         VDMC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (sumD + 1), s));
         dfree(g->nr_off, s);
         VDMC_CUDA(dalloc((void **)&g->nr_off, sizeof(int64_t) * (sumD + 1), s));
@@ -1324,7 +1324,7 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         size_t tb2 = 0;
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
         void *ts2 = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&ts2, tb2, s));
+        VDMC_CUDA(dalloc((void **)&ts2, tb2, s));
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts2, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
         count_launch(2);
         VDMC_CUDA(cudaMemcpyAsync(&g->nr_total, g->nr_off + sumD, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1334,15 +1334,15 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         k_nr<true><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, nullptr, g->nr_off,
                                            g->nr_adj, g->ctr + 3, cap);
         VDMC_LAUNCH();
-        cudaFreeAsync(ts2, s);
-        cudaFreeAsync(cnt, s);
-        cudaFreeAsync(dlist, s);
-        cudaFreeAsync(segs, s);
+        dfree(ts2, s);
+        dfree(cnt, s);
+        dfree(dlist, s);
+        dfree(segs, s);
     }
-    cudaFreeAsync(fh, s);
-    cudaFreeAsync(fl, s);
-    cudaFreeAsync(ft, s);
-    cudaFreeAsync(nsel, s);
+    dfree(fh, s);
+    dfree(fl, s);
+    dfree(ft, s);
+    dfree(nsel, s);
     VDMC_CUDA(cudaStreamSynchronize(s));
     g->nheavy = hn[0];
     g->nlight = hn[1];
@@ -1355,17 +1355,17 @@ vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t s) {
     if (!g->cost) VDMC_CUDA(dalloc((void **)&g->cost, sizeof(int64_t) * std::max<int64_t>(g->ntasks, 1), s));
     if (g->ntasks > 0) {
         int64_t *raw = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&raw, sizeof(int64_t) * g->ntasks, s));
+        VDMC_CUDA(dalloc((void **)&raw, sizeof(int64_t) * g->ntasks, s));
         k_cost<<<148 * 8, 256, 0, s>>>(g->ntasks, k, g->off, g->split, g->adj, g->tfirst, g->task_root, raw);
         VDMC_LAUNCH();
         size_t tb = 0;
         VDMC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, raw, g->cost, (int)g->ntasks, s));
         void *ts = nullptr;
-        VDMC_CUDA(cudaMallocAsync(&ts, tb, s));
+        VDMC_CUDA(dalloc((void **)&ts, tb, s));
         VDMC_CUDA(cub::DeviceScan::InclusiveSum(ts, tb, raw, g->cost, (int)g->ntasks, s));
         count_launch(2);
-        cudaFreeAsync(ts, s);
-        cudaFreeAsync(raw, s);
+        dfree(ts, s);
+        dfree(raw, s);
         VDMC_CUDA(cudaStreamSynchronize(s));
     }
     g->cost_k = k;

@@ -14,11 +14,13 @@ namespace vdmc {
 void set_error(const std::string &msg);
 vdmc_status fail(vdmc_status st, const char *fmt, ...);
 void count_launch(int n = 1);
-// Device memory: stream-ordered allocations from the device's default pool, which retains
-// freed memory (release threshold = max), so building and counting again reuses it instead of
-// paying cudaMalloc/cudaFree (page mapping of GB-sized count matrices) every call.
+// Device memory (api.cu): small buffers from the device's default stream-ordered pool; large
+// ones from a process-wide cache of blocks that are reused best-fit across calls and graphs
+// (no page mapping or pool fragmentation in a step).  Stream-ordered: dfree(p, s) makes the
+// block reusable after the work queued on s; a reuse on another stream waits for it.
 cudaError_t dalloc(void **p, size_t bytes, cudaStream_t s);
 void dfree(void *p, cudaStream_t s);
+void trim_cache(int dev);   // release the idle cached blocks of a device
 // Host-side trace (VDMC_TRACE=1): prints the host milliseconds since the previous point.
 void trace(const char *what);
 

@@ -21,7 +21,7 @@ STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASY
 EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_count", "vdmc_plan",
            "vdmc_split_costs", "vdmc_num_classes", "vdmc_class_ids", "vdmc_get_info",
            "vdmc_get_order", "vdmc_set_profiling", "vdmc_last_timings",
-           "vdmc_kernel_launches", "vdmc_free_graph", "vdmc_last_error"]
+           "vdmc_kernel_launches", "vdmc_free_graph", "vdmc_trim", "vdmc_last_error"]
 
 
 class VdmcError(RuntimeError):
@@ -68,6 +68,7 @@ def lib():
             "vdmc_last_timings": (_i32, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
             "vdmc_kernel_launches": (_i64, []),
             "vdmc_free_graph": (None, [_vp]),
+            "vdmc_trim": (_i32, [ctypes.c_int]),
             "vdmc_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -101,6 +102,11 @@ def split_costs(prefix: np.ndarray, nparts: int):
     parts = (Range * nparts)()
     _check(lib().vdmc_split_costs(prefix.ctypes.data if prefix.size else None, prefix.size, nparts, parts))
     return [(p.task_lo, p.task_hi) for p in parts]
+
+
+def trim(device: int = 0) -> None:
+    """Release the library's idle cached device blocks on `device` (vdmc_trim)."""
+    _check(lib().vdmc_trim(device))
 
 
 def kernel_launches() -> int:

@@ -217,3 +217,16 @@ def test_full_size_sampled_rows(vd, oracle_mod, name, k):
     verts = _sample_vertices(g, k, 24, 2e7, seed=int(name[3:]))
     want = oracle_mod.count_vertex(g, k, verts)
     assert np.array_equal(host[verts], want)
+
+
+def test_block_cache_reuse_and_trim(vd, oracle_mod):
+    """Large device buffers come from the library's block cache: graphs of different sizes
+    built and freed in turn reuse (and re-fit) cached blocks; results stay bit-exact, also
+    after vdmc_trim released the idle blocks."""
+    import torch
+    gs = [G.make_config("cfg3", scale=s) for s in (0.01, 0.004, 0.02)]
+    want = [oracle_mod.count_esu(g, 4) for g in gs]
+    for rep in range(2):
+        for g, w in zip(gs, want):
+            assert np.array_equal(gpu_count(vd, g, 4), w)
+        vd.trim(torch.cuda.current_device())
