@@ -65,7 +65,8 @@ struct Dev {
     int big;                                  // degrees so large a task could overflow u32 histograms
     int maxdeg;
     int off32;                                // n * C < 2^32: 32-bit accumulator offsets
-    int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop
+    int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
+    int fold;                                 // star chunks: fold the 16-bit counters every this many b (<= 65535)
     uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
     int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
     uint32_t ca_cap;
@@ -261,114 +262,28 @@ __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int
 }
 
 // ------------------------------------------------------------------ shape "3" at heavy roots
-// Loops interchanged: each lane owns two c's of a 64-position chunk of R, the warp walks
-// b = R[j], j in (i, pos(c)), uniformly.  Per iteration the warp reads codes[j] = code(r,b) |
-// code(a,b) << 2 (one byte) and R[j]; code(b, c) comes from the root's induced adjacency in
-// position space (pre-pass k_nr) through a per-c pointer; code(a, c) from Ba.  A set is
-// "plain" when code(a,b) = code(b,c) = 0 (almost every set at a hub); its mask, hence its
-// class, is then fixed by c's (code(r,c), code(a,c)) and the iteration's code(r,b), so
-//   * c counts its plain sets in 16-bit fields indexed by code(r,b); the classes are looked up
-//     once per c at the end of a block, where r and a (histogram H) and c are credited;
-//   * b gets, per key k = (code(r,c), code(a,c)) of c, popc(plain & M_k) sets of class
-//     lut[key k | code(r,b)]: lanes 0..11 own one key each, at most one atomic per lane;
-//   * the rare non-plain sets are classified one by one (star_slow).
-// Every set is visited once and classified through the LUT entry of its exact mask.
-struct StarC {
-    uint32_t c, lmask, npos, ncode;   // vertex, mask bits fixed by c, next induced neighbour of c
-    int64_t q, q1;                    // walk over c's induced adjacency
-    uint32_t pA, pB;                  // plain sets: pA = n(code(r,b)=1) | n(=2) << 16, pB = n(=3)
-    int key;                          // code(r,c) - 1 + 3 code(a,c); 15 = no c
-};
+// Task (r, a = R[i]); the star sets are {r, a, b = R[j], c = R[p]} with i < j < p.  A chunk
+// is W = 32 * kStarM consecutive c positions [cb, ce) (lane l, slot t owns p = cb + 32 t + l);
+// the warp walks b = R[j] for j in (i, ce) uniformly, one iteration = the chunk's sets with
+// that b.  Per iteration the warp reads R[j] (rank(b) << 2 | code(r, b)); code(a, b) comes
+// from codes[j] and code(b, c) from the root's induced adjacency in position space (pre-pass
+// k_nr) through a per-c pointer.  A set is "plain" when code(a, b) = code(b, c) = 0 (almost
+// every set at a hub: the induced graph of N+(r) has density ~2e-4 in cfg4); its mask, hence
+// its class, is then fixed by c's key (code(r, c), code(a, c)) and the iteration's code(r, b):
+//   * c side: the plain sets of every c with p > j get +1 in the field code(r, b) of a
+//     warp-uniform packed counter U (one add per iteration for the whole chunk); c takes its
+//     value when the walk reaches p (snapshot: U counts exactly the b before c), corrected by
+//     the per-c deltas of its non-plain sets;
+//   * b side: the key lanes (0..11) hold the number of chunk c's after b with their key and
+//     add it, in the class lut[key | code(r, b)], to b's row: one atomic per key present;
+//   * events (an a-b edge: every set of that b; a b-c edge: that c's set) are classified one
+//     by one through the LUT entry of their full mask (star_event).
+// Every set is counted once, in the class of its exact mask.  16-bit fields: U is folded into
+// the counts at least every g.fold iterations (65535).
+constexpr int kStarM = 4;                  // c slots per lane
+constexpr int kStarW = 32 * kStarM;        // c positions per star chunk
+constexpr uint32_t kInfPos = 0x3fffffffu;
 
-__device__ __forceinline__ void star_c_advance(const Dev &g, StarC &s) {
-    s.q++;
-    const uint32_t ne = s.q < s.q1 ? g.nr_adj[s.q] : 0xffffffffu;
-    s.npos = ne >> 2;
-    s.ncode = ne & 3u;
-}
-
-__device__ __forceinline__ void star_c_init(const Dev &g, StarC &s, const uint32_t *R, int D, const uint32_t *Ba,
-                                            uint32_t cra, int i, int p, int64_t seg) {
-    s.c = 0; s.lmask = 0; s.npos = 0x3fffffffu; s.ncode = 0; s.q = 0; s.q1 = 0; s.pA = 0; s.pB = 0; s.key = 15;
-    if (p < D && p >= i + 2) {
-        const uint32_t ec = R[p];
-        const uint32_t crc = ec & 3u, cac = get2(Ba, p);
-        s.c = ec >> 2;
-        s.lmask = cra | crc << 4 | cac << 8;
-        s.key = (int)(crc - 1u + 3u * cac);
-        s.q = g.nr_off[seg + p] - 1;
-        s.q1 = g.nr_off[seg + p + 1];
-        do star_c_advance(g, s);                        // first induced neighbour after a
-        while (s.npos <= (uint32_t)i);
-    }
-}
-
-template <int C>
-__device__ __forceinline__ void star_c_flush(const Dev &g, StarC &s, const uint8_t *lut, uint32_t *H) {
-    if (s.key == 15) return;
-    const uint32_t n[3] = {s.pA & 0xffffu, s.pA >> 16, s.pB};
-#pragma unroll
-    for (uint32_t crb = 1; crb <= 3; crb++) {
-        if (n[crb - 1]) {
-            const int col = lut[s.lmask | crb << 2];
-            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n[crb - 1]);
-            atomicAdd(H + col, n[crb - 1]);
-        }
-    }
-    s.pA = 0;
-    s.pB = 0;
-}
-
-// a set with an a-b or b-c edge: classify it alone
-template <int C>
-__device__ __forceinline__ void star_slow(const Dev &g, const StarC &s, const uint8_t *lut, uint32_t *H, uint32_t ub,
-                                          uint32_t b, bool hit) {
-    const uint32_t cbc = hit ? swap2(s.ncode) : 0u;   // the entry holds code(c, b)
-    const int col = lut[s.lmask | (ub & 3u) << 2 | (ub >> 2) << 6 | cbc << 10];
-    atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
-    atomicAdd(g.acc + (size_t)b * C + col, 1ull);
-    atomicAdd(H + col, 1u);
-}
-
-// b = R[j] for j in [j0, j1).  TAIL: some lanes' c are not after b (the chunk's own b's)
-template <int C, bool TAIL>
-__device__ __forceinline__ void star_run(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
-                                         const uint8_t *codes, StarC &s0, StarC &s1, int p0, int p1, unsigned M0,
-                                         unsigned M1, uint32_t kmask, int j0, int j1) {
-    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
-    for (int j = j0; j < j1; j++) {
-        const uint32_t ub = codes[j];
-        const uint32_t crb = ub & 3u;
-        const bool cabz = ub < 4u;
-        const uint32_t incA = crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u);
-        const uint32_t incB = crb == 3u ? 1u : 0u;
-        const bool h0 = s0.npos == (uint32_t)j, h1 = s1.npos == (uint32_t)j;
-        const bool v0 = TAIL ? (vc0 && p0 > j) : vc0;
-        const bool v1 = TAIL ? (vc1 && p1 > j) : vc1;
-        const bool pl0 = v0 && !h0 && cabz, pl1 = v1 && !h1 && cabz;
-        s0.pA += pl0 ? incA : 0u;
-        s0.pB += pl0 ? incB : 0u;
-        s1.pA += pl1 ? incA : 0u;
-        s1.pB += pl1 ? incB : 0u;
-        const unsigned bm0 = __ballot_sync(kFull, pl0), bm1 = __ballot_sync(kFull, pl1);
-        const uint32_t b = R[j] >> 2;
-        const unsigned cnt = __popc(bm0 & M0) + __popc(bm1 & M1);   // lanes >= 12 have M = 0
-        if (cnt) atomicAdd(g.acc + (size_t)b * C + lut[kmask | crb << 2], (unsigned long long)cnt);
-        const bool sl0 = v0 && !pl0, sl1 = v1 && !pl1;
-        if (__any_sync(kFull, sl0 || sl1 || h0 || h1)) {          // rare, warp-uniform
-            if (sl0) star_slow<C>(g, s0, lut, H, ub, b, h0);
-            if (sl1) star_slow<C>(g, s1, lut, H, ub, b, h1);
-            if (h0) star_c_advance(g, s0);
-            if (h1) star_c_advance(g, s1);
-        }
-    }
-}
-
-// Event-free iterations j in [j0, j1) of a star chunk: no a-b edge and no b-c edge for any
-// lane, so every valid lane's set is plain and the plain masks are the chunk's validity
-// masks.  Each iteration still enumerates its 64 sets {r, a, R[j], c}: c counts it in the
-// field of code(r, R[j]), and each key lane adds its (constant) number of c's to R[j] in the
-// class of (key, code(r, R[j])).
 // row offset of vertex v's column col in the accumulator (32-bit when n*C < 2^32)
 template <int C, bool OFF32>
 __device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, uint32_t col) {
@@ -376,106 +291,255 @@ __device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, 
     return g.acc + ((size_t)v * C + col);
 }
 
-template <int C, bool FULL, bool OFF32>
-__device__ __forceinline__ void star_fast_t(const Dev &g, const uint32_t *R, StarC &s0, StarC &s1, bool vc0,
-                                            bool vc1, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
-                                            int j0, int j1) {
-#pragma unroll 4
-    for (int j = j0; j < j1; j++) {
-        const uint32_t e = R[j];   // rank(b) << 2 | code(r, b)
-        const uint32_t crb = e & 3u;
-        const uint32_t incA = crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u);
-        const uint32_t incB = crb == 3u ? 1u : 0u;
-        if (FULL) {
-            s0.pA += incA;
-            s0.pB += incB;
-            s1.pA += incA;
-            s1.pB += incB;
-        } else {
-            s0.pA += vc0 ? incA : 0u;
-            s0.pB += vc0 ? incB : 0u;
-            s1.pA += vc1 ? incA : 0u;
-            s1.pB += vc1 ? incB : 0u;
+__device__ __forceinline__ uint32_t incA_of(uint32_t crb) { return crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u); }
+__device__ __forceinline__ uint32_t incB_of(uint32_t crb) { return crb == 3u ? 1u : 0u; }
+
+// c at position p: next entry of its induced list after index q with position < p, else INF
+__device__ __forceinline__ void nr_next(const Dev &g, int64_t seg, int p, uint32_t &q, uint32_t &npos) {
+    q++;
+    npos = kInfPos;
+    if ((int64_t)q < g.nr_off[seg + p + 1]) {
+        const uint32_t x = g.nr_adj[q] >> 2;
+        if ((int)x < p) npos = x;
+    }
+}
+
+struct StarS {
+    uint32_t dA[kStarM], dB[kStarM];   // per c: count deltas, then (after its snapshot) its counts
+    uint32_t npos[kStarM], q[kStarM];  // next event position of c, index of that induced entry
+    uint32_t keys;                     // 4 bits per slot: code(r,c) - 1 + 3 code(a,c); 15 = no c
+    uint32_t UA, UB;                   // warp-uniform plain counts: UA = n(crb=1) | n(crb=2) << 16, UB = n(crb=3)
+    unsigned cntk;                     // key lanes: chunk c's after the current b with this lane's key
+    uint32_t cols;                     // key lanes: column of (key | code(r,b)) in byte code(r,b)
+};
+
+template <int C>
+__device__ __forceinline__ void star_flush_c(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, uint32_t c,
+                                             uint32_t key, uint32_t fA, uint32_t fB) {
+    const uint32_t lmask = cra | ((key % 3u) + 1u) << 4 | (key / 3u) << 8;
+    const uint32_t n[3] = {fA & 0xffffu, fA >> 16, fB};
+#pragma unroll
+    for (uint32_t crb = 1; crb <= 3; crb++) {
+        if (n[crb - 1]) {
+            const int col = lut[lmask | crb << 2];
+            atomicAdd(g.acc + (size_t)c * C + col, (unsigned long long)n[crb - 1]);
+            atomicAdd(H + col, n[crb - 1]);
         }
-        if (cntk) {
-            const uint32_t col = crb == 1u ? col1 : (crb == 2u ? col2 : col3);
-            atomicAdd(acc_at<C, OFF32>(g, e >> 2, col), (unsigned long long)cntk);
+    }
+}
+
+// fold: the live c's (p >= j) add U and flush their counts; U restarts (16-bit fields)
+template <int C>
+__device__ __forceinline__ void star_fold(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, const uint32_t *R,
+                                          StarS &s, int cb, int ce, int j, int lane) {
+#pragma unroll
+    for (int t = 0; t < kStarM; t++) {
+        const int p = cb + 32 * t + lane;
+        if (p < ce && p >= j) {
+            star_flush_c<C>(g, lut, H, cra, R[p] >> 2, (s.keys >> (4 * t)) & 15u, s.dA[t] + s.UA, s.dB[t] + s.UB);
+            s.dA[t] = 0;
+            s.dB[t] = 0;
+        }
+    }
+    s.UA = 0;
+    s.UB = 0;
+}
+
+// the c at position j (>= cb) takes its snapshot; its key lane stops counting it for b's
+__device__ __forceinline__ void star_snapshot(StarS &s, int j, int cb, int lane) {
+    const int o = j - cb, owner = o & 31, ts = o >> 5;
+#pragma unroll
+    for (int t = 0; t < kStarM; t++) {
+        if (t == ts) {
+            if (lane == owner) {
+                s.dA[t] += s.UA;
+                s.dB[t] += s.UB;
+            }
+            const uint32_t kk = __shfl_sync(kFull, (s.keys >> (4 * t)) & 15u, owner);
+            if ((uint32_t)lane == kk) s.cntk--;
+        }
+    }
+}
+
+// iteration j with an event: an a-b edge (every set of b is classified alone) and/or b-c
+// edges (those c's sets are classified alone); the rest are plain
+template <int C>
+__device__ __forceinline__ void star_event(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra,
+                                           const uint32_t *R, const uint8_t *codes, int64_t seg, StarS &s, int j,
+                                           int cb, int ce, int lane) {
+    if (j >= cb) star_snapshot(s, j, cb, lane);
+    const uint32_t e = R[j], crb = e & 3u, b = e >> 2;
+    const uint32_t cab = (uint32_t)codes[j] >> 2;
+    const bool aev = cab != 0u;
+    unsigned nh = 0;   // key lanes: plain-count correction (hit c's with this key)
+#pragma unroll
+    for (int t = 0; t < kStarM; t++) {
+        const int p = cb + 32 * t + lane;
+        const bool valid = p < ce && p > j;
+        const bool hit = valid && s.npos[t] == (uint32_t)j;
+        const bool slow = valid && (aev || hit);
+        const uint32_t key = (s.keys >> (4 * t)) & 15u;
+        int col = kNone;
+        if (slow) {
+            const uint32_t cbc = hit ? swap2(g.nr_adj[s.q[t]] & 3u) : 0u;   // the entry holds code(c, b)
+            const uint32_t lmask = cra | ((key % 3u) + 1u) << 4 | (key / 3u) << 8;
+            col = lut[lmask | crb << 2 | cab << 6 | cbc << 10];
+            atomicAdd(g.acc + (size_t)(R[p] >> 2) * C + col, 1ull);
+            atomicAdd(H + col, 1u);
+            if (!aev) {   // U will count this j for every c: take it back for this one
+                s.dA[t] -= incA_of(crb);
+                s.dB[t] -= incB_of(crb);
+            }
+        }
+        const unsigned m = __match_any_sync(kFull, col);
+        if (col != kNone && lane == __ffs(m) - 1) atomicAdd(g.acc + (size_t)b * C + col, (unsigned long long)__popc(m));
+        if (!aev) {
+            for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
+                const uint32_t kk = __shfl_sync(kFull, key, __ffs(hm) - 1);
+                if ((uint32_t)lane == kk) nh++;
+            }
+        }
+        if (hit) nr_next(g, seg, p, s.q[t], s.npos[t]);
+    }
+    if (!aev) {
+        s.UA += incA_of(crb);
+        s.UB += incB_of(crb);
+        const unsigned cnt = s.cntk - nh;
+        if (cnt) atomicAdd(g.acc + (size_t)b * C + ((s.cols >> (crb << 3)) & 0xffu), (unsigned long long)cnt);
+    }
+}
+
+// event-free iterations [j0, j1): U counts, key lanes add to b's row; TAIL: snapshots
+template <int C, bool OFF32, bool TAIL>
+__device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarS &s, int j0, int j1, int cb,
+                                          int lane) {
+    if (!TAIL) {
+#pragma unroll 4
+        for (int j = j0; j < j1; j++) {
+            const uint32_t e = R[j];   // rank(b) << 2 | code(r, b)
+            const uint32_t crb = e & 3u;
+            s.UA += incA_of(crb);
+            s.UB += incB_of(crb);
+            if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
+                                  (unsigned long long)s.cntk);
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < kStarM; t++) {
+            const int a0 = max(j0, cb + 32 * t), a1 = min(j1, cb + 32 * t + 32);
+            const uint32_t kt = (s.keys >> (4 * t)) & 15u;
+            for (int j = a0; j < a1; j++) {
+                const int owner = j - cb - 32 * t;
+                if (lane == owner) {
+                    s.dA[t] += s.UA;
+                    s.dB[t] += s.UB;
+                }
+                if ((uint32_t)lane == __shfl_sync(kFull, kt, owner)) s.cntk--;
+                const uint32_t e = R[j];
+                const uint32_t crb = e & 3u;
+                s.UA += incA_of(crb);
+                s.UB += incB_of(crb);
+                if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
+                                      (unsigned long long)s.cntk);
+            }
         }
     }
 }
 
 template <int C>
-__device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarC &s0, StarC &s1, bool vc0, bool vc1,
-                                          bool full, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
-                                          int j0, int j1) {
-    if (j0 >= j1) return;
-    if (g.off32) {
-        if (full) star_fast_t<C, true, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
-        else star_fast_t<C, false, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
-    } else {
-        star_fast_t<C, false, false>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
+__device__ __forceinline__ void star_fast_any(const Dev &g, const uint32_t *R, StarS &s, int j0, int j1, int cb,
+                                              int lane) {
+    const int f1 = min(j1, cb);
+    if (j0 < f1) {
+        if (g.off32) star_fast<C, true, false>(g, R, s, j0, f1, cb, lane);
+        else star_fast<C, false, false>(g, R, s, j0, f1, cb, lane);
+    }
+    const int t0 = max(j0, cb);
+    if (t0 < j1) {
+        if (g.off32) star_fast<C, true, true>(g, R, s, t0, j1, cb, lane);
+        else star_fast<C, false, true>(g, R, s, t0, j1, cb, lane);
     }
 }
 
-// chunk k of the task (r, a = R[i]): c positions [max(D - 64(k+1), i+2), D - 64k), the
-// longest chunks first.  AP[0..nap) = positions of R adjacent to a (nap < 0: unknown).
+// first j' in [j, jend) with an a-b edge (codes[j'] >= 4), else jend
+__device__ __forceinline__ int next_a_event(const uint8_t *codes, int j, int jend, int lane) {
+    for (int base = j; base < jend; base += 32) {
+        const int p = base + lane;
+        const unsigned m = __ballot_sync(kFull, p < jend && codes[p] >= 4);
+        if (m) return base + __ffs(m) - 1;
+    }
+    return jend;
+}
+
+// chunk k of the task (r, a = R[i]): c positions [max(D - W(k+1), i+2), D - W k), the longest
+// chunks first
 template <int C>
 __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
-                                           uint32_t *H, const uint32_t *AP, int nap, int k, int lane) {
+                                           uint32_t *H, int k, int lane) {
     const int64_t seg = g.hbase[r];
-    const int cb = D - 64 * (k + 1);
-    const int p0 = cb + lane, p1 = cb + 32 + lane;
-    StarC s0, s1;
-    star_c_init(g, s0, R, D, Ba, cra, i, p0, seg);
-    star_c_init(g, s1, R, D, Ba, cra, i, p1, seg);
-    unsigned M0 = 0, M1 = 0;
+    const int ce = D - kStarW * k, cb = max(ce - kStarW, i + 2);
+    StarS s;
+    s.keys = 0;
 #pragma unroll
-    for (int q = 0; q < 12; q++) {
-        const unsigned m0 = __ballot_sync(kFull, s0.key == q), m1 = __ballot_sync(kFull, s1.key == q);
-        if (lane == q) { M0 = m0; M1 = m1; }
-    }
-    const uint32_t kmask = cra | ((uint32_t)(lane % 3) + 1u) << 4 | ((uint32_t)(lane / 3) & 3u) << 8;
-    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
-    const bool full = __all_sync(kFull, vc0 && vc1);
-    const unsigned cntk = __popc(M0) + __popc(M1);   // key lanes: the chunk's c's with that key
-    uint32_t col1 = 0, col2 = 0, col3 = 0;
-    if (cntk) {
-        col1 = lut[kmask | 1u << 2];
-        col2 = lut[kmask | 2u << 2];
-        col3 = lut[kmask | 3u << 2];
-    }
-    const int jmain = max(i + 1, min(cb, D));           // b before every c of the chunk
-    const int pmax = D - 64 * k - 1;                     // last c position of the chunk
-    int ap = 0;
-    if (nap > 0)
-        while (ap < nap && (int)AP[ap] <= i) ap++;
-    // 16-bit fields: flush at least every 65535 iterations
-    for (int jb = i + 1; jb < jmain; jb += 65535) {
-        const int je = min(jmain, jb + 65535);
-        if (nap < 0) {
-            star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jb, je);
-        } else {
-            int j = jb;
-            while (j < je) {
-                const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next b-c edge
-                const int eva = ap < nap ? (int)AP[ap] : je;                            // next a-b edge
-                const int stop = min(je, min((int)min(evw, 0x3fffffffu), eva));
-                star_fast<C>(g, R, s0, s1, vc0, vc1, full, cntk, col1, col2, col3, j, stop);
-                j = stop;
-                if (j < je) {   // an event: one general iteration
-                    star_run<C, false>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, j, j + 1);
-                    if (j == eva) ap++;
-                    j++;
-                }
-            }
+    for (int t = 0; t < kStarM; t++) {
+        const int p = cb + 32 * t + lane;
+        s.dA[t] = 0;
+        s.dB[t] = 0;
+        s.npos[t] = kInfPos;
+        s.q[t] = 0;
+        uint32_t key = 15u;
+        if (p < ce) {
+            const uint32_t ec = R[p];
+            key = (ec & 3u) - 1u + 3u * get2(Ba, p);
+            s.q[t] = (uint32_t)g.nr_off[seg + p] - 1u;
+            do nr_next(g, seg, p, s.q[t], s.npos[t]);   // first induced neighbour after a
+            while (s.npos[t] <= (uint32_t)i);
         }
-        star_c_flush<C>(g, s0, lut, H);
-        star_c_flush<C>(g, s1, lut, H);
+        s.keys |= key << (4 * t);
     }
-    star_run<C, true>(g, lut, H, R, codes, s0, s1, p0, p1, M0, M1, kmask, jmain, pmax);
-    star_c_flush<C>(g, s0, lut, H);
-    star_c_flush<C>(g, s1, lut, H);
+    s.cntk = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 12; q++) {
+        unsigned cnt = 0;
+#pragma unroll
+        for (int t = 0; t < kStarM; t++) cnt += __popc(__ballot_sync(kFull, ((s.keys >> (4 * t)) & 15u) == q));
+        if ((uint32_t)lane == q) s.cntk = cnt;
+    }
+    s.cols = 0;
+    if (s.cntk) {
+        const uint32_t kmask = cra | ((uint32_t)(lane % 3) + 1u) << 4 | ((uint32_t)(lane / 3) & 3u) << 8;
+        s.cols = (uint32_t)lut[kmask | 1u << 2] << 8 | (uint32_t)lut[kmask | 2u << 2] << 16 |
+                 (uint32_t)lut[kmask | 3u << 2] << 24;
+    }
+    s.UA = 0;
+    s.UB = 0;
+    int j = i + 1;
+    int anext = next_a_event(codes, j, ce, lane);
+    int jfold = j + g.fold;
+    while (j < ce) {
+        uint32_t cm = s.npos[0];
+#pragma unroll
+        for (int t = 1; t < kStarM; t++) cm = min(cm, s.npos[t]);
+        const int cev = (int)min(__reduce_min_sync(kFull, cm), kInfPos);
+        const int stop = min(min(ce, jfold), min(anext, cev));
+        star_fast_any<C>(g, R, s, j, stop, cb, lane);
+        j = stop;
+        if (j >= ce) break;
+        if (j == jfold) {
+            star_fold<C>(g, lut, H, cra, R, s, cb, ce, j, lane);
+            jfold = j + g.fold;
+            continue;
+        }
+        star_event<C>(g, lut, H, cra, R, codes, seg, s, j, cb, ce, lane);
+        j++;
+        if (anext < j) anext = next_a_event(codes, j, ce, lane);
+    }
+#pragma unroll
+    for (int t = 0; t < kStarM; t++) {
+        const int p = cb + 32 * t + lane;
+        if (p < ce) star_flush_c<C>(g, lut, H, cra, R[p] >> 2, (s.keys >> (4 * t)) & 15u, s.dA[t], s.dB[t]);
+    }
     if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
     __syncwarp();
 }
@@ -928,14 +992,14 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                             lane);
     } else {
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
-        const bool cross = ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
-        const int nch = D - (i + 2) > 0 ? (D - (i + 2) + 63) / 64 : 0;          // star chunks
+        const bool cross = !(g.skip & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
+        const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
         const int nck = (nL + 63) / 64, njb = (D + kCrossBlock - 1) / kCrossBlock;
         const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
         const int total = nch + nB + nL;
         // longest first across kinds: star chunks longer than a cross block, the "2+1" items,
         // the remaining star chunks, then the b-in-L_a items
-        const int nlong = cross ? max(0, min(nch, (D - i - 2 - kCrossBlock) / 64 + 1)) : nch;
+        const int nlong = cross ? max(0, min(nch, (D - i - 2 - kCrossBlock) / kStarW + 1)) : nch;
         for (;;) {
             int it = 0;
             if (lane == 0) it = atomicAdd(wctr, 1);
@@ -946,7 +1010,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             else if (it < nlong + nB) b_it = it - nlong;
             else if (it < nch + nB) star_k = it - nB;
             if (star_k >= 0) {
-                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, AP, nap, star_k, lane);
+                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, lane);
             } else if (b_it >= 0) {
                 if (g.skip & 2) continue;
                 if (cross)
@@ -1428,6 +1492,10 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     }
     if (const char *sk = getenv("VDMC_SKIP")) {   // profiling only; results incomplete
         d.skip = atoi(sk);
+    }
+    d.fold = 65535;
+    if (const char *fo = getenv("VDMC_FOLD")) {   // tests: exercise the fold path on small graphs
+        d.fold = std::max(1, std::min(65535, atoi(fo)));
     }
     d.acc = (unsigned long long *)g->acc;
     d.gheavy = g->lscratch;

@@ -89,7 +89,7 @@ def test_rank_invariance(vd, oracle_mod, k):
 
 
 @pytest.mark.parametrize("k", [3, 4])
-@pytest.mark.parametrize("mode", ["smem", "global", "random-rank"])
+@pytest.mark.parametrize("mode", ["smem", "global", "random-rank", "fold"])
 def test_heavy_and_light_paths(vd, oracle_mod, k, mode, monkeypatch):
     """A graph with roots on both sides of the light/heavy threshold (G_U degree 256): heavy
     tasks with buffers in shared memory, forced into the global-memory fallback, and a random
@@ -99,6 +99,8 @@ def test_heavy_and_light_paths(vd, oracle_mod, k, mode, monkeypatch):
     assert deg.max() > 300
     if mode == "global":
         monkeypatch.setenv("VDMC_HEAVY_GLOBAL", "1")
+    if mode == "fold":   # star chunks fold their 16-bit counters every 37 b's instead of 65535
+        monkeypatch.setenv("VDMC_FOLD", "37")
     rank = np.random.default_rng(3).permutation(g[0]) if mode == "random-rank" else None
     assert np.array_equal(gpu_count(vd, g, k, rank=rank), oracle_mod.count_esu(g, k))
 

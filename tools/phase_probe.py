@@ -19,7 +19,9 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("skip b in L_a", {"VDMC_SKIP": "4"}), ("heavy, skip star", {"VDMC_PHASES": "1", "VDMC_SKIP": "1"}),
             ("heavy, skip b in R", {"VDMC_PHASES": "1", "VDMC_SKIP": "2"}),
             ("heavy, skip b in L_a", {"VDMC_PHASES": "1", "VDMC_SKIP": "4"}),
-            ("heavy, skip all", {"VDMC_PHASES": "1", "VDMC_SKIP": "7"})]
+            ("heavy, skip all", {"VDMC_PHASES": "1", "VDMC_SKIP": "7"}),
+            ("no cross items (fallback)", {"VDMC_SKIP": "8"}),
+            ("heavy, skip all, no ca_build", {"VDMC_PHASES": "1", "VDMC_SKIP": "15"})]
 for label, env in variants:
     for key in ("VDMC_PHASES", "VDMC_SKIP"):
         os.environ.pop(key, None)
