@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--config", default="cfg4", choices=sorted(G.CONFIGS))
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--impl", default="vdmc", choices=["vdmc", "reference"])
+    p.add_argument("--kind", default="directed", choices=["directed", "undirected"],
+                   help="motif kind (undirected = SURVEY 8(f) NEXT-1); the headline is directed")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -231,7 +233,7 @@ def main():
         g = vdmc.Graph(n, e_src, e_dst, device=local)
         g.set_profiling(True)
         work = g.plan(k, world)[rank] if world > 1 else None
-        out = g.count(k, work=work)
+        out = g.count(k, work=work, kind=args.kind)
         if world > 1:
             dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
         if out_host is not None and rank == 0:
@@ -283,7 +285,7 @@ def main():
     # ---- e2e: pinned host edges -> public API -> host count matrix
     h_src = torch.from_numpy(src).pin_memory()
     h_dst = torch.from_numpy(dst).pin_memory()
-    C = vdmc.num_classes(k)
+    C = vdmc.num_classes(k, args.kind)
     h_out = torch.empty((n, C), dtype=torch.int64).pin_memory() if rank == 0 else None
 
     def e2e_step():
@@ -346,7 +348,7 @@ def main():
             "edges_per_sec": arcs / (ms_per_step / 1e3),
             "motifs_per_step": total_sets,
             "config": {"workload": f"{args.config}: {G.CONFIGS[args.config]['desc']}", "k": k, "n": n,
-                       "arcs": arcs, "parallelism": f"dp{world} (graph replicated, task slices, NCCL reduce)"
+                       "arcs": arcs, "motif_kind": args.kind, "parallelism": f"dp{world} (graph replicated, task slices, NCCL reduce)"
                        if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write); count matrix >> L2"},
             "kernel_ms": {"enum_avg": enum_avg, "step_avg": ms_per_step, "enum_share": enum_avg / ms_per_step,

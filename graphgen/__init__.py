@@ -31,7 +31,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = [
-    "gnp_directed", "ba_directed", "CONFIGS", "make_config", "config_seed",
+    "gnp_directed", "gnp_undirected", "ba_directed", "CONFIGS", "make_config", "config_seed",
     "complete_digraph", "transitive_tournament", "directed_cycle", "out_star",
     "in_star", "directed_path", "dag_grid", "undirected_cycle", "paper_example",
     "random_small", "relabel", "transpose", "make_mutual",
@@ -86,6 +86,14 @@ def gnp_directed(n: int, p: float, seed: int):
     w = pos % (n - 1)
     v = w + (w >= u)
     return _finish(n, u, v)
+
+
+def gnp_undirected(n: int, p: float, seed: int):
+    """Undirected G(n, p): each of the C(n, 2) unordered pairs independently with
+    prob. p, emitted as one arc u -> v with u < v (the undirected motif count ignores it)."""
+    n, s, d = gnp_directed(n, p, seed)
+    keep = s < d                          # an ordered-pair G(n,p) restricted to u < v
+    return n, s[keep], d[keep]
 
 
 def ba_directed(n: int, m: int, seed: int, rho: float = 0.1):

@@ -49,6 +49,14 @@ enum {
 
 typedef struct vdmc_graph vdmc_graph;   /* opaque; immutable after build except for scratch */
 
+/* Motif kind.  VDMC_DIRECTED: the classes above.  VDMC_UNDIRECTED:
+ * undirected motifs "in the undirected graph induced by ignoring the direction of edges"
+ * (G_U): a connected k-set's class is that of its G_U-induced subgraph, indexed by
+ * the paper's index of its symmetric adjacency matrix (reading G17), so the
+ * columns are the all-mutual directed classes: k = 3 -> [23, 63] (path, triangle); k = 4 ->
+ * [591, 669, 735, 1782, 1791, 4095] (star, path, paw, 4-cycle, diamond, clique). */
+enum { VDMC_DIRECTED = 0, VDMC_UNDIRECTED = 1 };
+
 /* A contiguous slice [task_lo, task_hi) of the graph's task list.  A task is one
  * (root r, depth-1 neighbour a) pair with rank(a) > rank(r): the paper's unit of GPU work,
  * "each pair of a vertex and one of its neighbors is computed separately".
@@ -96,6 +104,12 @@ vdmc_status vdmc_build_graph(int64_t n, const int64_t *indptr, const int32_t *nb
 vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
                        void *stream);
 
+/* vdmc_count for either motif kind: counts is device uint64 [n][vdmc_num_classes_kind(k, kind)].
+ * Same enumeration, slices and semantics as vdmc_count; only the class table differs.
+ * Errors: as vdmc_count, plus VDMC_EINVAL for kind not in {VDMC_DIRECTED, VDMC_UNDIRECTED}. */
+vdmc_status vdmc_count_kind(vdmc_graph *g, int k, int kind, uint64_t *counts, const vdmc_range *work,
+                            void *stream);
+
 /* Cost-balanced split of the task list into nparts contiguous slices:
  * parts[p] for p in [0, nparts).  Uses a per-task cost proxy computed on the device
  * (synchronous).  Errors: VDMC_EK, VDMC_EINVAL (nparts < 1 or parts NULL), VDMC_ECUDA. */
@@ -112,6 +126,11 @@ int vdmc_num_classes(int k);
 /* ids[j] = canonical (minimum) paper index of column j, ascending (reading G9).
  * ids: host uint16 [vdmc_num_classes(k)].  Errors: VDMC_EK, VDMC_EINVAL. */
 vdmc_status vdmc_class_ids(int k, uint16_t *ids);
+
+/* Class count / column ids for a motif kind: 13 / 199 (directed), 2 / 6 (undirected); -1 (or
+ * VDMC_EK / VDMC_EINVAL) for a bad k or kind. */
+int vdmc_num_classes_kind(int k, int kind);
+vdmc_status vdmc_class_ids_kind(int k, int kind, uint16_t *ids);
 
 /* Graph facts (host struct). */
 vdmc_status vdmc_get_info(const vdmc_graph *g, vdmc_graph_info *info);

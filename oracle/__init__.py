@@ -18,6 +18,13 @@ Contents (each function cites the PAPER.md passage it follows; see
                        (tiny graphs only; shares nothing with the C file).
 * ``expected_gnp``   — Eq. 4, expected per-vertex count in G(n, p).
 * ``n_iso``          — N_Iso(m): isomorph count per class.
+* ``symmetrize`` / ``undirected_class_ids`` / ``count_undirected`` — undirected motifs
+                       (counted "in the undirected graph induced by ignoring the
+                       direction of edges", G_U of P:76): the directed definition applied to
+                       the all-mutual graph of G_U, columns = the all-mutual classes.
+* ``count_py_undirected`` — pure-Python brute force for undirected motifs, classes named by
+                       (edge count, degree sequence) (shares nothing with the C file).
+* ``expected_gnp_undirected`` — Eq. 4 with the undirected n_max = C(k, 2).
 
 Every function is pinned by ``tests/test_oracle_*.py`` (closed forms, the
 hand-worked golden of the paper's example graph, single-motif graphs,
@@ -213,3 +220,110 @@ def expected_gnp(k: int, n: int, p: float) -> np.ndarray:
     ne = n_edges(k)
     nmax = k * (k - 1)
     return math.comb(n - 1, k - 1) * n_iso(k) * p ** ne * (1.0 - p) ** (nmax - ne)
+
+
+# ------------------------------------------------------------------ undirected motifs
+def symmetrize(g):
+    """G_U as a directed graph ("ignoring the direction of the edge"): every arc u -> v
+    becomes the mutual pair u <-> v (duplicates merged)."""
+    n, s, d = g
+    s = np.asarray(s, np.int64)
+    d = np.asarray(d, np.int64)
+    a = np.concatenate([s, d])
+    b = np.concatenate([d, s])
+    key = np.unique(a * n + b) if a.size else np.zeros(0, np.int64)
+    return n, (key // n).astype(np.int32), (key % n).astype(np.int32)
+
+
+def undirected_class_ids(k: int) -> np.ndarray:
+    """Canonical ids of the undirected k-motifs: the paper's index of a symmetric
+    adjacency matrix, minimised over vertex orders -- i.e. the connected classes whose
+    minimum-index matrix is symmetric (reading G17)."""
+    t = class_table(k)
+    pairs = [(i, j) for i in range(k) for j in range(k) if i != j]
+    nb = len(pairs)
+    out = []
+    for cid in t["class_ids"]:
+        bits = {pairs[b] for b in range(nb) if (int(cid) >> (nb - 1 - b)) & 1}
+        if all((j, i) in bits for (i, j) in bits):
+            out.append(int(cid))
+    return np.array(out, np.int64)
+
+
+def count_undirected(g, k: int, method: str = "esu") -> np.ndarray:
+    """Undirected per-vertex k-motif counts: every connected k-set S, class of the
+    G_U-induced subgraph, +1 for every member.  Written as the directed definition on
+    symmetrize(g) -- whose induced subgraphs are exactly the symmetric matrices of G_U[S] --
+    restricted to the all-mutual columns.  method: "esu" or "brute"."""
+    sym = symmetrize(g)
+    full = count_esu(sym, k) if method == "esu" else count_brute(sym, k)
+    ids = list(class_table(k)["class_ids"])
+    cols = [ids.index(c) for c in undirected_class_ids(k)]
+    return np.ascontiguousarray(full[:, cols])
+
+
+def count_vertex_undirected(g, k: int, verts) -> np.ndarray:
+    """Rows of sampled vertices of count_undirected (per-vertex ESU on symmetrize(g))."""
+    ids = list(class_table(k)["class_ids"])
+    cols = [ids.index(c) for c in undirected_class_ids(k)]
+    return np.ascontiguousarray(count_vertex(symmetrize(g), k, verts)[:, cols])
+
+
+# (edge count, sorted degree sequence) names every connected graph on 3 or 4 vertices
+UNDIRECTED_NAMES = {
+    3: {(2, (1, 1, 2)): "path", (3, (2, 2, 2)): "triangle"},
+    4: {(3, (1, 1, 1, 3)): "star", (3, (1, 1, 2, 2)): "path", (4, (1, 2, 2, 3)): "paw",
+        (4, (2, 2, 2, 2)): "cycle", (5, (2, 2, 3, 3)): "diamond", (6, (3, 3, 3, 3)): "clique"},
+}
+
+
+def count_py_undirected(g, k: int):
+    """Pure-Python brute force: {(v, name): count} over connected k-sets of G_U, the class
+    named by its edge count and degree sequence (no index, no table)."""
+    n, s, d = g
+    und = {frozenset(e) for e in zip(s.tolist(), d.tolist())}
+    out: dict = {}
+    for S in itertools.combinations(range(n), k):
+        es = [(x, y) for x, y in itertools.combinations(S, 2) if frozenset((x, y)) in und]
+        comp, grew = {S[0]}, True
+        while grew:
+            grew = False
+            for x, y in es:
+                if (x in comp) != (y in comp):
+                    comp |= {x, y}
+                    grew = True
+        if len(comp) < k:
+            continue
+        deg = tuple(sorted(sum(v in e for e in es) for v in S))
+        name = UNDIRECTED_NAMES[k][(len(es), deg)]
+        for v in S:
+            out[(v, name)] = out.get((v, name), 0) + 1
+    return out
+
+
+def n_iso_undirected(k: int) -> np.ndarray:
+    """Labelled undirected graphs per undirected class (the undirected N_Iso of P:187)."""
+    return np.array([_n_sym_masks(k, int(c)) for c in undirected_class_ids(k)])
+
+
+def _n_sym_masks(k: int, cid: int) -> int:
+    """Symmetric indices whose minimum over vertex orders is cid (labelled undirected graphs)."""
+    t = class_table(k)
+    pairs = [(i, j) for i in range(k) for j in range(k) if i != j]
+    nb = len(pairs)
+    cnt = 0
+    for m in range(1 << nb):
+        bits = {pairs[b] for b in range(nb) if (m >> (nb - 1 - b)) & 1}
+        if all((j, i) in bits for (i, j) in bits) and t["conn"][m] and int(t["canon"][m]) == cid:
+            cnt += 1
+    return cnt
+
+
+def expected_gnp_undirected(k: int, n: int, p: float) -> np.ndarray:
+    """Eq. 4 for an undirected G(n, p): n_max = C(k, 2), N_Iso the
+    labelled undirected graphs of the class, n_e its edge count."""
+    ids = undirected_class_ids(k)
+    ne = np.array([bin(int(c)).count("1") // 2 for c in ids])
+    iso = n_iso_undirected(k)
+    nmax = k * (k - 1) // 2
+    return math.comb(n - 1, k - 1) * iso * p ** ne * (1.0 - p) ** (nmax - ne)

@@ -169,7 +169,11 @@ static int paper_index(int k, const int adj[4][4], const int *perm) {
     return idx;
 }
 
-static void build_table(int k, ClassTable &t) {
+// kind 1 (undirected motifs, "count undirected sub-graph in the undirected graph induced
+// by ignoring the direction"; reading G17): a set's class is that of its G_U-induced subgraph,
+// i.e. every pair with an arc in either direction is an edge both ways; its index is the
+// paper's index of that symmetric adjacency matrix.
+static void build_table(int k, int kind, ClassTable &t) {
     static const int P3[3][2] = {{0, 1}, {0, 2}, {1, 2}};
     static const int P4[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
     const int npairs = k == 3 ? 3 : 6;
@@ -182,6 +186,7 @@ static void build_table(int k, ClassTable &t) {
         int und[4][4] = {};
         for (int p = 0; p < npairs; p++) {
             int c = (m >> (2 * p)) & 3, x = pairs[p][0], y = pairs[p][1];
+            if (kind == 1 && c) c = 3;
             if (c & 1) adj[x][y] = 1;
             if (c & 2) adj[y][x] = 1;
             if (c) und[x][y] = und[y][x] = 1;
@@ -215,20 +220,24 @@ static void build_table(int k, ClassTable &t) {
             t.lut[m] = (uint8_t)(std::lower_bound(ids.begin(), ids.end(), canon[m]) - ids.begin());
 }
 
-static ClassTable g_tab[2];
+static ClassTable g_tab[4];
 static std::once_flag g_tab_once;
 
-static const ClassTable &table(int k) {
+static const ClassTable &table(int k, int kind) {
     std::call_once(g_tab_once, [] {
-        build_table(3, g_tab[0]);
-        build_table(4, g_tab[1]);
+        for (int kd = 0; kd < 2; kd++) {
+            build_table(3, kd, g_tab[2 * kd]);
+            build_table(4, kd, g_tab[2 * kd + 1]);
+        }
     });
-    return g_tab[k == 3 ? 0 : 1];
+    return g_tab[2 * kind + (k == 3 ? 0 : 1)];
 }
 
-const uint8_t *host_lut(int k) { return table(k).lut.data(); }
-const uint16_t *host_class_ids(int k) { return table(k).ids.data(); }
-int num_classes(int k) { return (k == 3 || k == 4) ? (int)table(k).ids.size() : -1; }
+const uint8_t *host_lut(int k, int kind) { return table(k, kind).lut.data(); }
+const uint16_t *host_class_ids(int k, int kind) { return table(k, kind).ids.data(); }
+int num_classes(int k, int kind) {
+    return (k == 3 || k == 4) && (kind == 0 || kind == 1) ? (int)table(k, kind).ids.size() : -1;
+}
 
 }  // namespace vdmc
 
@@ -241,14 +250,19 @@ const char *vdmc_last_error(void) { return g_err.c_str(); }
 
 int64_t vdmc_kernel_launches(void) { return g_launches.load(); }
 
-int vdmc_num_classes(int k) { return vdmc::num_classes(k); }
+int vdmc_num_classes(int k) { return vdmc::num_classes(k, VDMC_DIRECTED); }
 
-vdmc_status vdmc_class_ids(int k, uint16_t *ids) {
+int vdmc_num_classes_kind(int k, int kind) { return vdmc::num_classes(k, kind); }
+
+vdmc_status vdmc_class_ids_kind(int k, int kind, uint16_t *ids) {
     if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
+    if (kind != VDMC_DIRECTED && kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", kind);
     if (!ids) return fail(VDMC_EINVAL, "ids is NULL");
-    memcpy(ids, host_class_ids(k), sizeof(uint16_t) * num_classes(k));
+    memcpy(ids, host_class_ids(k, kind), sizeof(uint16_t) * num_classes(k, kind));
     return VDMC_OK;
 }
+
+vdmc_status vdmc_class_ids(int k, uint16_t *ids) { return vdmc_class_ids_kind(k, VDMC_DIRECTED, ids); }
 
 static vdmc_status check_device(int device) {
     int nd = 0;
@@ -369,8 +383,9 @@ vdmc_status vdmc_get_order(const vdmc_graph *g, int32_t *order) {
     return VDMC_OK;
 }
 
-vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work, void *stream) {
+vdmc_status vdmc_count_kind(vdmc_graph *g, int k, int kind, uint64_t *counts, const vdmc_range *work, void *stream) {
     if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
+    if (kind != VDMC_DIRECTED && kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", kind);
     if (!g) return fail(VDMC_EINVAL, "graph is NULL");
     if (!counts && g->n > 0) return fail(VDMC_EINVAL, "counts is NULL");
     int64_t lo = 0, hi = g->ntasks;
@@ -382,7 +397,11 @@ vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range 
         hi = work->task_hi;
     }
     VDMC_CUDA(cudaSetDevice(g->device));
-    return launch_count(g, k, counts, lo, hi, (cudaStream_t)stream);
+    return launch_count(g, k, kind, counts, lo, hi, (cudaStream_t)stream);
+}
+
+vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work, void *stream) {
+    return vdmc_count_kind(g, k, VDMC_DIRECTED, counts, work, stream);
 }
 
 vdmc_status vdmc_split_costs(const int64_t *prefix, int64_t ntasks, int nparts, vdmc_range *parts) {
@@ -460,7 +479,7 @@ void vdmc_free_graph(vdmc_graph *g) {
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
     void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->acc,
-                    g->lscratch, g->ctr, g->lut3, g->lut4, g->cost, g->heavy_task, g->light_root,
+                    g->lscratch, g->ctr, g->lut[0][0], g->lut[0][1], g->lut[1][0], g->lut[1][1], g->cost, g->heavy_task, g->light_root,
                     g->hroots, g->hbase, g->nr_off, g->nr_adj};
     for (void *p : ptrs) dfree(p, nullptr);
     cudaStreamSynchronize(nullptr);

@@ -261,6 +261,79 @@ __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int
     return nL;
 }
 
+// Phase A of a heavy task, by the whole CTA: a's list in 32-entry groups, warp w takes groups
+// w, w + NW, ...  Pass 1 scatters code(a, x), x in R, into Ba and records per group the ballots
+// of its L_a entries and of its entries in R; warp 0 scans the group counts; pass 2 writes La
+// (sorted: list order) and AP (positions of R adjacent to a, ascending, first kAPcap).
+// tmp: 4 * ceil(len / 32) words of zeroed scratch, NOT re-zeroed here (the caller clears it).
+// *s_nL = |L_a|, *s_nap = |AP| (may exceed kAPcap).  Ends with a barrier.
+template <int NW>
+__device__ void build_a_cta(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
+                            uint32_t *AP, uint32_t *tmp, int *s_nL, int *s_nap, int wid, int lane) {
+    const int G = (al.len + 31) >> 5;
+    uint32_t *KM = tmp, *AM = tmp + G, *KO = tmp + 2 * G, *AO = tmp + 3 * G;
+    for (int gi = wid; gi < G; gi += NW) {
+        const int p = gi * 32 + lane;
+        bool keep = false, inR = false;
+        if (p < al.len) {
+            const uint32_t e = al.p[p], x = e >> 2;
+            if (x > r) {
+                const int pos = find_rank(R, D, x);
+                if (pos >= 0) {
+                    set2(Ba, pos, e & 3u);
+                    inR = true;
+                } else {
+                    keep = true;
+                }
+            }
+        }
+        const unsigned km = __ballot_sync(kFull, keep), am = __ballot_sync(kFull, inR);
+        if (lane == 0) {
+            KM[gi] = km;
+            AM[gi] = am;
+        }
+    }
+    __syncthreads();
+    if (wid == 0) {
+        int bk = 0, ba = 0;
+        for (int g0 = 0; g0 < G; g0 += 32) {
+            const int gi = g0 + lane;
+            const int ck = gi < G ? __popc(KM[gi]) : 0, ca = gi < G ? __popc(AM[gi]) : 0;
+            int ik = ck, ia = ca;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int yk = __shfl_up_sync(kFull, ik, d), ya = __shfl_up_sync(kFull, ia, d);
+                if (lane >= d) {
+                    ik += yk;
+                    ia += ya;
+                }
+            }
+            if (gi < G) {
+                KO[gi] = (uint32_t)(bk + ik - ck);
+                AO[gi] = (uint32_t)(ba + ia - ca);
+            }
+            bk += __shfl_sync(kFull, ik, 31);
+            ba += __shfl_sync(kFull, ia, 31);
+        }
+        if (lane == 0) {
+            *s_nL = bk;
+            *s_nap = ba;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int gi = wid; gi < G; gi += NW) {
+        const unsigned km = KM[gi], am = AM[gi];
+        const int p = gi * 32 + lane;
+        if (km >> lane & 1u) La[KO[gi] + __popc(km & lt)] = al.p[p];
+        if (am >> lane & 1u) {
+            const uint32_t slot = AO[gi] + __popc(am & lt);
+            if (slot < (uint32_t)kAPcap) AP[slot] = (uint32_t)find_rank(R, D, al.p[p] >> 2);
+        }
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ shape "3" at heavy roots
 // Task (r, a = R[i]); the star sets are {r, a, b = R[j], c = R[p]} with i < j < p.  A chunk
 // is W = 32 * kStarM consecutive c positions [cb, ce) (lane l, slot t owns p = cb + 32 t + l);
@@ -948,13 +1021,12 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
 // NW == 1: one warp does everything in order.  NW > 1 (heavy): the CTA's warps take work
 // items from the shared counter *wctr (star chunks longest first, then b in R, then b in L_a).
 // Bb/Bl are this warp's scratch bitmaps (zero on entry and exit), H its histogram.
-template <int K, int NW>
+template <int K, int C, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
                                            int *s_ca, const Staged *st, const uint32_t *AP, int nap, int w,
                                            int lane) {
-    constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
@@ -1028,10 +1100,9 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
     }
 }
 
-template <int K, bool HSMEM>
+template <int K, int C, bool HSMEM>
 __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo, int64_t hi,
                                                      unsigned long long *ctr, const uint8_t *__restrict__ lut_g) {
-    constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
     constexpr int NM = K == 3 ? 64 : 4096;
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
@@ -1072,23 +1143,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 staged = r;
                 __syncthreads();
             }
-            if (wid == 0) {
-                int nap = 0;
-                const int nL = build_a(g, r, glist(g, R[i] >> 2), R, D, Ba, La, lane, AP, &nap);
-                if (lane == 0) {
-                    s_nap = nap;
-                    s_nL = nL;
-                    s_work = 0;
-                    s_ca = 0;
-                }
-            }
-            __syncthreads();
+            const List al = glist(g, R[i] >> 2);
+            build_a_cta<kWarps>(g, r, al, R, D, Ba, La, AP, hb + L.Bl, &s_nL, &s_nap, wid, lane);
             const int nL = s_nL;
-            if (K == 4) {   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2
-                for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
-                __syncthreads();
+            for (int q = tid; q < 4 * ((al.len + 31) >> 5); q += kBlock) hb[L.Bl + q] = 0;   // build_a_cta scratch
+            if (tid == 0) {
+                s_work = 0;
+                s_ca = 0;
             }
-            task_loops<K, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
+            if (K == 4)   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2
+                for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
+            __syncthreads();
+            task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
                                   g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, nullptr, AP,
                                   s_nap <= kAPcap ? s_nap : -1, wid, lane);
             flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
@@ -1136,7 +1202,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 }
                 const int nL = build_a(g, r, al, R, D, Ba, La, lane);
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kLcap, lane);
-                task_loops<K, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
+                task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
                                  nullptr, -1, 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
@@ -1283,8 +1349,8 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
 
 }  // namespace
 
-vdmc_status ensure_acc(vdmc_graph *g, int k, cudaStream_t s) {
-    const int C = num_classes(k);
+vdmc_status ensure_acc(vdmc_graph *g, int k, int kind, cudaStream_t s) {
+    const int C = num_classes(k, kind);
     const size_t need = (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t);
     if (g->acc_bytes < need) {
         dfree(g->acc, s);
@@ -1294,13 +1360,11 @@ vdmc_status ensure_acc(vdmc_graph *g, int k, cudaStream_t s) {
         g->acc_bytes = need;
     }
     if (!g->ctr) VDMC_CUDA(dalloc((void **)&g->ctr, 4 * sizeof(unsigned long long), s));
-    if (!g->lut3) {
-        VDMC_CUDA(dalloc((void **)&g->lut3, 64, s));
-        VDMC_CUDA(cudaMemcpyAsync(g->lut3, host_lut(3), 64, cudaMemcpyHostToDevice, s));
-    }
-    if (!g->lut4) {
-        VDMC_CUDA(dalloc((void **)&g->lut4, 4096, s));
-        VDMC_CUDA(cudaMemcpyAsync(g->lut4, host_lut(4), 4096, cudaMemcpyHostToDevice, s));
+    uint8_t *&lut = g->lut[kind][k == 4 ? 1 : 0];
+    if (!lut) {
+        const size_t nm = k == 3 ? 64 : 4096;
+        VDMC_CUDA(dalloc((void **)&lut, nm, s));
+        VDMC_CUDA(cudaMemcpyAsync(lut, host_lut(k, kind), nm, cudaMemcpyHostToDevice, s));
     }
     return VDMC_OK;
 }
@@ -1436,9 +1500,9 @@ vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t s) {
     return VDMC_OK;
 }
 
-template <int K>
-static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, cudaStream_t s) {
-    constexpr int C = K == 3 ? kNumClasses3 : kNumClasses4;
+template <int K, int C>
+static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int64_t lo, int64_t hi,
+                       cudaStream_t s) {
     const int dev = g->device;
     int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1454,7 +1518,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     const char *force = getenv("VDMC_HEAVY_GLOBAL");
     const Layout L = make_layout((int)g->max_degree, C, heavy_in_smem, per_cta, force && force[0] == '1');
     const size_t smem = (size_t)L.total * 4;
-    auto kern = heavy_in_smem ? k_enum<K, true> : k_enum<K, false>;
+    auto kern = heavy_in_smem ? k_enum<K, C, true> : k_enum<K, C, false>;
     VDMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
@@ -1513,7 +1577,7 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
     if (hi > lo) {
-        kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, K == 3 ? g->lut3 : g->lut4);
+        kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, lut);
         VDMC_LAUNCH();
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[2], s));
@@ -1529,12 +1593,16 @@ static vdmc_status run(vdmc_graph *g, uint64_t *counts, int64_t lo, int64_t hi, 
     return VDMC_OK;
 }
 
-vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi, cudaStream_t s) {
+vdmc_status launch_count(vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
+                         cudaStream_t s) {
     trace("count start");
-    vdmc_status st = ensure_acc(g, k, s);
+    vdmc_status st = ensure_acc(g, k, kind, s);
     if (st) return st;
     trace("ensure_acc");
-    return k == 3 ? run<3>(g, counts, lo, hi, s) : run<4>(g, counts, lo, hi, s);
+    const uint8_t *lut = g->lut[kind][k == 4 ? 1 : 0];
+    if (kind == VDMC_UNDIRECTED)
+        return k == 3 ? run<3, kNumClassesU3>(g, lut, counts, lo, hi, s) : run<4, kNumClassesU4>(g, lut, counts, lo, hi, s);
+    return k == 3 ? run<3, kNumClasses3>(g, lut, counts, lo, hi, s) : run<4, kNumClasses4>(g, lut, counts, lo, hi, s);
 }
 
 }  // namespace vdmc

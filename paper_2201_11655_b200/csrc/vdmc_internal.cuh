@@ -48,13 +48,16 @@ void trace(const char *what);
 // (1,2),(1,3),(2,3) [k=4] or (0,1),(0,2),(1,2) [k=3] occupies bits 2p..2p+1 with
 //   bit 2p   = first -> second,   bit 2p+1 = second -> first.
 // The host LUT maps every such mask to the column of its minimum-isomorph paper index.
+// kind 0 = directed motifs, 1 = undirected motifs (classes of the G_U-induced subgraph)
 constexpr int kNumClasses3 = 13;
 constexpr int kNumClasses4 = 199;
+constexpr int kNumClassesU3 = 2;
+constexpr int kNumClassesU4 = 6;
 constexpr uint8_t kNoClass = 255;
 
-const uint8_t *host_lut(int k);          // [64] or [4096]
-const uint16_t *host_class_ids(int k);   // [13] or [199]
-int num_classes(int k);
+const uint8_t *host_lut(int k, int kind);          // [64] or [4096]
+const uint16_t *host_class_ids(int k, int kind);   // [13] / [199], undirected [2] / [6]
+int num_classes(int k, int kind);
 
 }  // namespace vdmc
 
@@ -76,7 +79,7 @@ struct vdmc_graph {
     uint32_t *lscratch = nullptr;  // per-warp depth-2 candidate lists
     size_t lscratch_elems = 0;
     unsigned long long *ctr = nullptr;   // work counter(s)
-    uint8_t *lut3 = nullptr, *lut4 = nullptr;
+    uint8_t *lut[2][2] = {};        // [kind][k == 4] device class LUTs
     int64_t *cost = nullptr;       // [ntasks] inclusive prefix of the plan's cost proxy
     int cost_k = 0;
     // schedule: tasks of heavy roots (CTA per task) and light roots (warp per root), rank order
@@ -102,8 +105,8 @@ struct vdmc_graph {
 namespace vdmc {
 vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst,
                          const int32_t *h_rank, int device, cudaStream_t stream, vdmc_graph *g);
-vdmc_status ensure_acc(vdmc_graph *g, int k, cudaStream_t s);
+vdmc_status ensure_acc(vdmc_graph *g, int k, int kind, cudaStream_t s);
 vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t stream);
-vdmc_status launch_count(vdmc_graph *g, int k, uint64_t *counts, int64_t lo, int64_t hi,
+vdmc_status launch_count(vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
                          cudaStream_t stream);
 }  // namespace vdmc

@@ -18,8 +18,9 @@ STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASY
           5: "VDMC_EORDER", 6: "VDMC_EK", 7: "VDMC_ENOMEM", 8: "VDMC_ECUDA", 9: "VDMC_ENODEV"}
 
 # Every symbol include/vdmc.h declares (tests check the .so exports exactly these)
-EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_count", "vdmc_plan",
-           "vdmc_split_costs", "vdmc_num_classes", "vdmc_class_ids", "vdmc_get_info",
+EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_count", "vdmc_count_kind", "vdmc_plan",
+           "vdmc_split_costs", "vdmc_num_classes", "vdmc_class_ids", "vdmc_num_classes_kind",
+           "vdmc_class_ids_kind", "vdmc_get_info",
            "vdmc_get_order", "vdmc_set_profiling", "vdmc_last_timings",
            "vdmc_kernel_launches", "vdmc_free_graph", "vdmc_trim", "vdmc_last_error"]
 
@@ -58,6 +59,9 @@ def lib():
                                               ctypes.POINTER(_vp)]),
             "vdmc_build_graph": (_i32, [_i64, _vp, _vp, _vp, _vp, ctypes.c_int, ctypes.POINTER(_vp)]),
             "vdmc_count": (_i32, [_vp, ctypes.c_int, _vp, ctypes.POINTER(Range), _vp]),
+            "vdmc_count_kind": (_i32, [_vp, ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(Range), _vp]),
+            "vdmc_num_classes_kind": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+            "vdmc_class_ids_kind": (_i32, [ctypes.c_int, ctypes.c_int, _vp]),
             "vdmc_plan": (_i32, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Range)]),
             "vdmc_split_costs": (_i32, [_vp, _i64, ctypes.c_int, ctypes.POINTER(Range)]),
             "vdmc_num_classes": (ctypes.c_int, [ctypes.c_int]),
@@ -84,16 +88,27 @@ def _check(st):
         raise VdmcError(st, lib().vdmc_last_error().decode())
 
 
-def num_classes(k: int) -> int:
-    return lib().vdmc_num_classes(k)
+DIRECTED, UNDIRECTED = 0, 1
+_KINDS = {"directed": DIRECTED, "undirected": UNDIRECTED, DIRECTED: DIRECTED, UNDIRECTED: UNDIRECTED}
 
 
-def class_ids(k: int) -> np.ndarray:
-    C = num_classes(k)
+def _kind(kind) -> int:
+    if kind not in _KINDS:
+        raise ValueError(f"motif kind {kind!r} not in ('directed', 'undirected')")
+    return _KINDS[kind]
+
+
+def num_classes(k: int, kind="directed") -> int:
+    return lib().vdmc_num_classes_kind(k, _kind(kind))
+
+
+def class_ids(k: int, kind="directed") -> np.ndarray:
+    kd = _kind(kind)
+    C = num_classes(k, kd)
     if C < 0:
-        _check(lib().vdmc_class_ids(k, None))
+        _check(lib().vdmc_class_ids_kind(k, kd, None))
     out = np.zeros(C, np.uint16)
-    _check(lib().vdmc_class_ids(k, out.ctypes.data))
+    _check(lib().vdmc_class_ids_kind(k, kd, out.ctypes.data))
     return out
 
 
@@ -183,12 +198,14 @@ class Graph:
         _check(lib().vdmc_get_order(self._h, out.ctypes.data))
         return out[: self.n]
 
-    def count(self, k: int, out=None, work=None, stream=None):
-        """uint64 counts [n][C] as an int64 torch tensor on the graph's device (same bits)."""
+    def count(self, k: int, out=None, work=None, stream=None, kind="directed"):
+        """uint64 counts [n][C] as an int64 torch tensor on the graph's device (same bits).
+        kind: "directed" (13 / 199 classes) or "undirected" (2 / 6 classes of G_U)."""
         import torch
-        C = num_classes(k)
+        kd = _kind(kind)
+        C = num_classes(k, kd)
         if C < 0:
-            _check(lib().vdmc_count(self._h, k, None, None, None))
+            _check(lib().vdmc_count_kind(self._h, k, kd, None, None, None))
         if out is None:
             out = torch.empty((self.n, C), dtype=torch.int64, device=f"cuda:{self.device}")
         assert out.is_cuda and out.dtype == torch.int64 and out.is_contiguous() and out.shape == (self.n, C)
@@ -196,8 +213,8 @@ class Graph:
         if work is not None:
             rng = Range(int(work[0]), int(work[1]))
         with torch.cuda.device(self.device):
-            _check(lib().vdmc_count(self._h, k, out.data_ptr() if out.numel() else None,
-                                    ctypes.byref(rng) if rng is not None else None, _stream_ptr(stream)))
+            _check(lib().vdmc_count_kind(self._h, k, kd, out.data_ptr() if out.numel() else None,
+                                         ctypes.byref(rng) if rng is not None else None, _stream_ptr(stream)))
         return out
 
     def plan(self, k: int, nparts: int):
@@ -225,17 +242,17 @@ class Graph:
             pass
 
 
-def count(n: int, src, dst, k: int, device: int = 0, rank=None):
+def count(n: int, src, dst, k: int, device: int = 0, rank=None, kind="directed"):
     """One-shot: build the graph on `device`, count k-motifs, return a host uint64 [n][C]."""
     g = Graph(n, src, dst, rank=rank, device=device)
     try:
-        out = g.count(k)
+        out = g.count(k, kind=kind)
         return out.cpu().numpy().view(np.uint64)
     finally:
         g.close()
 
 
-def count_distributed(g: Graph, k: int, group=None, dst_rank: int = 0):
+def count_distributed(g: Graph, k: int, group=None, dst_rank: int = 0, kind="directed"):
     """Multi-GPU: the graph is replicated on every rank; rank p counts the
     p-th cost-balanced slice of the (root, neighbour) task list into a private partial; one
     NCCL reduce (sum over int64 = the same bits as uint64 wrap-around addition) gives the full
@@ -244,6 +261,6 @@ def count_distributed(g: Graph, k: int, group=None, dst_rank: int = 0):
     world = dist.get_world_size(group)
     me = dist.get_rank(group)
     parts = g.plan(k, world)
-    out = g.count(k, work=parts[me])
+    out = g.count(k, work=parts[me], kind=kind)
     dist.reduce(out, dst=dst_rank, op=dist.ReduceOp.SUM, group=group)
     return out

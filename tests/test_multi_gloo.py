@@ -29,7 +29,7 @@ class OracleSliceGraph:
     def plan(self, k, nparts):
         return self.vdmc.split_costs(self.prefix, nparts)
 
-    def count(self, k, work=None):
+    def count(self, k, work=None, kind="directed"):
         lo, hi = work if work is not None else (0, self.g[0])
         out = self.oracle.count_esu(self.g, k, lo, hi, threads=1)
         return torch.from_numpy(out.view(np.int64).copy())
