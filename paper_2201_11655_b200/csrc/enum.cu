@@ -89,8 +89,8 @@ constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 // per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
 constexpr int kAPcap = 1024;                 // heavy: positions of R adjacent to a, kept for the fast loops
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
-constexpr int kLcap = 320;                   // light: staged list entries (R's lists, L_a's lists)
-constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + 2 * kLcap;
+constexpr int kPool = 960;                   // light: staged list entries, R's lists then L_a's lists
+constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool;
 
 __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x) {
     // position of vertex x in the sorted entry list S[0..len), or -1
@@ -728,239 +728,172 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
 
 // ------------------------------------------------------------------ "2+1" at heavy roots
 // For the task (r, x = R[i]) both kinds of "2+1" set containing x are enumerated with lanes =
-// c in L_x (two per lane: 64-wide chunks of L_x) and a warp-uniform walk over positions j of R:
-//   j > i:  {r, a = x, b = R[j], c}, c in L_a             (every j)
-//   j < i:  {r, a = R[j], b = x, c}, c in L_b \ N(a)      (only if R[j] is not adjacent to c)
+// c in L_x (kStarM per lane: 128-wide chunks of L_x) and a warp-uniform walk over positions j
+// of R (one item = a chunk of c's x a block of kCrossBlock positions):
+//   PART 2, j < i:  {r, a = R[j], b = x, c}, c in L_b \ N(a)   (only if R[j] is not adjacent to c)
+//   PART 1, j > i:  {r, a = x, b = R[j], c}, c in L_a          (every j)
 // Together these are exactly the "2+1" sets whose first or second depth-1 vertex is x, each
 // once (the set {r, a < b, c} is met in the task of a if c ~ a, else in the task of b).
 // code(R[j], c) comes from c's R-neighbour list, built per task in CTA scratch (ca_build).
 // As in the star loop, a plain set (no x-R[j] edge and no R[j]-c edge) has its class fixed by
-// c's code(x, c) and the iteration's code(r, R[j]): c and the pair (r, x) accumulate per-lane
-// 16-bit counters, R[j] gets popc(plain & M_k) per key k = code(x, c) from lanes 0..2, and
-// the remaining sets are classified one by one (cross_slow).
-constexpr int kCrossBlock = 1024;   // j-block length (< 2^16: the per-lane 16-bit counters)
+// c's key code(x, c) and the iteration's code(r, R[j]): every c counts it in the warp-uniform
+// U, corrected per c at its events; R[j] gets, from key lanes 0..2, the number of the chunk's
+// c's with that key; an x-R[j] edge makes every set of that j non-plain (classified alone), an
+// R[j]-c edge makes c's PART 1 set non-plain and removes its PART 2 set (c is in N(a)).
+constexpr int kCrossBlock = 1024;   // j-block length (< 2^16: the 16-bit count fields)
 
-struct CrossC {
-    uint32_t c, cxc, npos, ncode, q, q1;
-    uint32_t f1A, f1B, f2A, f2B;   // plain sets for j > i / j < i: A = n(crj=1) | n(crj=2) << 16, B = n(crj=3)
-    int key;                       // code(x, c) - 1; 15 = no c
-};
-
-__device__ __forceinline__ void cross_c_next(const uint32_t *CA, CrossC &s) {
-    const uint32_t e = s.q < s.q1 ? CA[s.q] : 0xffffffffu;
-    s.npos = e >> 2;
-    s.ncode = e & 3u;
+// c's R-neighbour list pointer: next entry (position of R, code(c, R[pos])) with position < jend
+__device__ __forceinline__ void ca_next(const uint32_t *CA, uint32_t q1, uint32_t &q, uint32_t &npos) {
+    q++;
+    npos = q < q1 ? CA[q] >> 2 : kInfPos;
 }
 
-__device__ __forceinline__ void cross_c_init(CrossC &s, const uint32_t *La, int nL, const uint32_t *CAbeg,
-                                             const uint32_t *CAlen, const uint32_t *CA, int q, int j0) {
-    s.c = 0; s.cxc = 0; s.npos = 0x3fffffffu; s.ncode = 0; s.q = 0; s.q1 = 0;
-    s.f1A = 0; s.f1B = 0; s.f2A = 0; s.f2B = 0; s.key = 15;
-    if (q < nL) {
-        const uint32_t e = La[q];
-        s.c = e >> 2;
-        s.cxc = e & 3u;
-        s.key = (int)s.cxc - 1;
-        s.q = CAbeg[q];
-        s.q1 = s.q + CAlen[q];
-        cross_c_next(CA, s);
-        while (s.npos < (uint32_t)j0) {
-            s.q++;
-            cross_c_next(CA, s);
-        }
-    }
-}
-
-template <int C>
-__device__ __forceinline__ void cross_c_flush(const Dev &g, CrossC &s, const uint8_t *lut, uint32_t *H, uint32_t cra) {
-    if (s.key == 15) return;
-    const uint32_t n1[3] = {s.f1A & 0xffffu, s.f1A >> 16, s.f1B};
-    const uint32_t n2[3] = {s.f2A & 0xffffu, s.f2A >> 16, s.f2B};
+template <int C, int PART>
+__device__ __forceinline__ void cross_flush(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra,
+                                            const uint32_t *La, int q0, int nL, StarS &s, int lane) {
 #pragma unroll
-    for (uint32_t crj = 1; crj <= 3; crj++) {
-        if (n1[crj - 1]) {   // (r, x, R[j], c)
-            const int col = lut[cra | crj << 2 | s.cxc << 8];
-            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n1[crj - 1]);
-            atomicAdd(H + col, n1[crj - 1]);
+    for (int t = 0; t < kStarM; t++) {
+        const int q = q0 + 32 * t + lane;
+        if (q < nL) {
+            const uint32_t ec = La[q], c = ec >> 2, cxc = ec & 3u;
+            const uint32_t fA = s.dA[t] + s.UA, fB = s.dB[t] + s.UB;
+            const uint32_t n[3] = {fA & 0xffffu, fA >> 16, fB};
+#pragma unroll
+            for (uint32_t crj = 1; crj <= 3; crj++) {
+                if (n[crj - 1]) {
+                    const int col = PART == 1 ? lut[cra | crj << 2 | cxc << 8] : lut[crj | cra << 2 | cxc << 10];
+                    atomicAdd(g.acc + (size_t)c * C + col, (unsigned long long)n[crj - 1]);
+                    atomicAdd(H + col, n[crj - 1]);
+                }
+            }
         }
-        if (n2[crj - 1]) {   // (r, R[j], x, c)
-            const int col = lut[crj | cra << 2 | s.cxc << 10];
-            atomicAdd(g.acc + (size_t)s.c * C + col, (unsigned long long)n2[crj - 1]);
-            atomicAdd(H + col, n2[crj - 1]);
-        }
+        s.dA[t] = 0;
+        s.dB[t] = 0;
     }
-    s.f1A = 0; s.f1B = 0; s.f2A = 0; s.f2B = 0;
+    s.UA = 0;
+    s.UB = 0;
 }
 
-// a non-plain set: PART 1 (j > i) with an x-R[j] or R[j]-c edge, PART 2 (j < i) with an
-// x-R[j] edge (and no R[j]-c edge)
+// positions [j0, j1) of one part (all c's of the chunk valid throughout)
 template <int C, int PART>
-__device__ __forceinline__ void cross_slow(const Dev &g, const CrossC &s, const uint8_t *lut, uint32_t *H, uint32_t ub,
-                                           uint32_t cra, uint32_t b, bool hit) {
-    const uint32_t crj = ub & 3u, cxj = ub >> 2;   // code(r, R[j]), code(x, R[j])
-    int col;
-    if (PART == 1) {
-        const uint32_t cjc = hit ? swap2(s.ncode) : 0u;   // the entry holds code(c, R[j])
-        col = lut[cra | crj << 2 | cxj << 6 | s.cxc << 8 | cjc << 10];
-    } else {
-        col = lut[crj | cra << 2 | swap2(cxj) << 6 | s.cxc << 10];
-    }
-    atomicAdd(g.acc + (size_t)s.c * C + col, 1ull);
-    atomicAdd(g.acc + (size_t)b * C + col, 1ull);
-    atomicAdd(H + col, 1u);
-}
-
-template <int C, int PART>
-__device__ __forceinline__ void cross_run(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
-                                          const uint8_t *codes, const uint32_t *CA, CrossC &s0, CrossC &s1,
-                                          unsigned M0, unsigned M1, uint32_t cra, int j0, int j1, int lane) {
-    const uint32_t kc = (uint32_t)lane + 1u;   // lanes 0..2 own key code(x, c) = lane + 1
-    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
-    for (int j = j0; j < j1; j++) {
-        const uint32_t ub = codes[j];
-        const uint32_t crj = ub & 3u;
-        const bool cz = ub < 4u;                    // no x-R[j] edge
-        const uint32_t incA = crj == 1u ? 1u : (crj == 2u ? 0x10000u : 0u);
-        const uint32_t incB = crj == 3u ? 1u : 0u;
-        const bool h0 = s0.npos == (uint32_t)j, h1 = s1.npos == (uint32_t)j;
-        const bool pl0 = vc0 && !h0 && cz, pl1 = vc1 && !h1 && cz;
-        if (PART == 1) {
-            s0.f1A += pl0 ? incA : 0u;
-            s0.f1B += pl0 ? incB : 0u;
-            s1.f1A += pl1 ? incA : 0u;
-            s1.f1B += pl1 ? incB : 0u;
-        } else {
-            s0.f2A += pl0 ? incA : 0u;
-            s0.f2B += pl0 ? incB : 0u;
-            s1.f2A += pl1 ? incA : 0u;
-            s1.f2B += pl1 ? incB : 0u;
-        }
-        const unsigned bm0 = __ballot_sync(kFull, pl0), bm1 = __ballot_sync(kFull, pl1);
-        const unsigned cnt = __popc(bm0 & M0) + __popc(bm1 & M1);   // lanes >= 3 have M = 0
-        if (cnt) {
-            const int col = PART == 1 ? lut[cra | crj << 2 | kc << 8] : lut[crj | cra << 2 | kc << 10];
-            atomicAdd(g.acc + (size_t)(R[j] >> 2) * C + col, (unsigned long long)cnt);
-        }
-        const bool sl0 = vc0 && !pl0 && (PART == 1 || !h0), sl1 = vc1 && !pl1 && (PART == 1 || !h1);
-        if (__any_sync(kFull, sl0 || sl1 || h0 || h1)) {   // rare, warp-uniform
-            const uint32_t b = R[j] >> 2;
-            if (sl0) cross_slow<C, PART>(g, s0, lut, H, ub, cra, b, h0);
-            if (sl1) cross_slow<C, PART>(g, s1, lut, H, ub, cra, b, h1);
-            if (h0) { s0.q++; cross_c_next(CA, s0); }
-            if (h1) { s1.q++; cross_c_next(CA, s1); }
-        }
-    }
-}
-
-// Event-free iterations j in [j0, j1) of a cross item (no x-R[j] edge, no R[j]-c edge for any
-// lane): every valid lane's set is plain; c counts it in the field of code(r, R[j]) and the
-// key lanes add their constant count to R[j].
-template <int C, int PART, bool FULL, bool OFF32>
-__device__ __forceinline__ void cross_fast_t(const Dev &g, const uint32_t *R, CrossC &s0, CrossC &s1, bool vc0,
-                                             bool vc1, unsigned cntk, uint32_t col1, uint32_t col2, uint32_t col3,
-                                             int j0, int j1) {
-#pragma unroll 4
-    for (int j = j0; j < j1; j++) {
-        const uint32_t e = R[j];   // rank(R[j]) << 2 | code(r, R[j])
-        const uint32_t crj = e & 3u;
-        const uint32_t incA = crj == 1u ? 1u : (crj == 2u ? 0x10000u : 0u);
-        const uint32_t incB = crj == 3u ? 1u : 0u;
-        uint32_t &a0 = PART == 1 ? s0.f1A : s0.f2A, &b0 = PART == 1 ? s0.f1B : s0.f2B;
-        uint32_t &a1 = PART == 1 ? s1.f1A : s1.f2A, &b1 = PART == 1 ? s1.f1B : s1.f2B;
-        if (FULL) {
-            a0 += incA;
-            b0 += incB;
-            a1 += incA;
-            b1 += incB;
-        } else {
-            a0 += vc0 ? incA : 0u;
-            b0 += vc0 ? incB : 0u;
-            a1 += vc1 ? incA : 0u;
-            b1 += vc1 ? incB : 0u;
-        }
-        if (cntk) {
-            const uint32_t col = crj == 1u ? col1 : (crj == 2u ? col2 : col3);
-            atomicAdd(acc_at<C, OFF32>(g, e >> 2, col), (unsigned long long)cntk);
-        }
-    }
-}
-
-template <int C, int PART>
-__device__ __forceinline__ void cross_fast(const Dev &g, const uint32_t *R, CrossC &s0, CrossC &s1, bool vc0,
-                                           bool vc1, bool full, unsigned cntk, uint32_t col1, uint32_t col2,
-                                           uint32_t col3, int j0, int j1) {
+__device__ __forceinline__ void cross_part(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra,
+                                           const uint32_t *R, const uint8_t *codes, const uint32_t *La, int q0,
+                                           int nL, const uint32_t *CAbeg, const uint32_t *CAlen, const uint32_t *CA,
+                                           StarS &s, int j0, int j1, int lane) {
     if (j0 >= j1) return;
-    if (g.off32) {
-        if (full) cross_fast_t<C, PART, true, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
-        else cross_fast_t<C, PART, false, true>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
-    } else {
-        cross_fast_t<C, PART, false, false>(g, R, s0, s1, vc0, vc1, cntk, col1, col2, col3, j0, j1);
-    }
-}
-
-// positions [j0, j1) of one part: event-free runs in cross_fast, events in cross_run
-template <int C, int PART>
-__device__ __forceinline__ void cross_span(const Dev &g, const uint8_t *lut, uint32_t *H, const uint32_t *R,
-                                           const uint8_t *codes, const uint32_t *CA, CrossC &s0, CrossC &s1,
-                                           unsigned M0, unsigned M1, uint32_t cra, const uint32_t *AP, int nap,
-                                           int j0, int j1, int lane) {
-    if (j0 >= j1) return;
-    if (nap < 0) {
-        cross_run<C, PART>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j0, j1, lane);
-        return;
-    }
-    const bool vc0 = s0.key != 15, vc1 = s1.key != 15;
-    const bool full = __all_sync(kFull, vc0 && vc1);
-    const unsigned cntk = __popc(M0) + __popc(M1);
     const uint32_t kc = (uint32_t)lane + 1u;
-    uint32_t col1 = 0, col2 = 0, col3 = 0;
-    if (cntk) {
-        col1 = PART == 1 ? lut[cra | 1u << 2 | kc << 8] : lut[1u | cra << 2 | kc << 10];
-        col2 = PART == 1 ? lut[cra | 2u << 2 | kc << 8] : lut[2u | cra << 2 | kc << 10];
-        col3 = PART == 1 ? lut[cra | 3u << 2 | kc << 8] : lut[3u | cra << 2 | kc << 10];
+    s.cols = 0;
+    if (s.cntk) {
+        s.cols = PART == 1 ? ((uint32_t)lut[cra | 1u << 2 | kc << 8] << 8 | (uint32_t)lut[cra | 2u << 2 | kc << 8] << 16 |
+                              (uint32_t)lut[cra | 3u << 2 | kc << 8] << 24)
+                           : ((uint32_t)lut[1u | cra << 2 | kc << 10] << 8 | (uint32_t)lut[2u | cra << 2 | kc << 10] << 16 |
+                              (uint32_t)lut[3u | cra << 2 | kc << 10] << 24);
     }
-    int ap = 0;
-    while (ap < nap && (int)AP[ap] < j0) ap++;
     int j = j0;
+    int anext = next_a_event(codes, j, j1, lane);
     while (j < j1) {
-        const uint32_t evw = __reduce_min_sync(kFull, min(s0.npos, s1.npos));   // next R[j]-c edge
-        const int eva = ap < nap ? (int)AP[ap] : j1;                            // next x-R[j] edge
-        const int stop = min(j1, min((int)min(evw, 0x3fffffffu), eva));
-        cross_fast<C, PART>(g, R, s0, s1, vc0, vc1, full, cntk, col1, col2, col3, j, stop);
-        j = stop;
-        if (j < j1) {
-            cross_run<C, PART>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, j, j + 1, lane);
-            if (j == eva) ap++;
-            j++;
+        uint32_t cm = s.npos[0];
+#pragma unroll
+        for (int t = 1; t < kStarM; t++) cm = min(cm, s.npos[t]);
+        const int cev = (int)min(__reduce_min_sync(kFull, cm), kInfPos);
+        const int stop = min(j1, min(anext, cev));
+        if (j < stop) {
+            if (g.off32) star_fast<C, true, false>(g, R, s, j, stop, 0, lane);
+            else star_fast<C, false, false>(g, R, s, j, stop, 0, lane);
         }
+        j = stop;
+        if (j >= j1) break;
+        // event at j
+        const uint32_t e = R[j], crj = e & 3u, b = e >> 2;
+        const uint32_t cxj = (uint32_t)codes[j] >> 2;   // code(x, R[j])
+        const bool aev = cxj != 0u;
+        unsigned nh = 0;
+#pragma unroll
+        for (int t = 0; t < kStarM; t++) {
+            const int q = q0 + 32 * t + lane;
+            const bool valid = q < nL;
+            const bool hit = valid && s.npos[t] == (uint32_t)j;
+            int col = kNone;
+            uint32_t c = 0;
+            const bool slow = PART == 1 ? valid && (aev || hit) : valid && aev && !hit;
+            if (slow) {
+                const uint32_t ec = La[q], cxc = ec & 3u;
+                c = ec >> 2;
+                if (PART == 1) {
+                    const uint32_t cjc = hit ? swap2(CA[s.q[t]] & 3u) : 0u;   // the entry holds code(c, R[j])
+                    col = lut[cra | crj << 2 | cxj << 6 | cxc << 8 | cjc << 10];
+                } else {
+                    col = lut[crj | cra << 2 | swap2(cxj) << 6 | cxc << 10];
+                }
+                atomicAdd(g.acc + (size_t)c * C + col, 1ull);
+                atomicAdd(H + col, 1u);
+            }
+            if (hit && !aev) {   // U will count this j for every c: take it back for this one
+                s.dA[t] -= incA_of(crj);
+                s.dB[t] -= incB_of(crj);
+            }
+            const unsigned m = __match_any_sync(kFull, col);
+            if (col != kNone && lane == __ffs(m) - 1) atomicAdd(g.acc + (size_t)b * C + col, (unsigned long long)__popc(m));
+            if (!aev) {
+                const uint32_t key = valid ? (La[q] & 3u) - 1u : 15u;
+                for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
+                    const uint32_t kk = __shfl_sync(kFull, key, __ffs(hm) - 1);
+                    if ((uint32_t)lane == kk) nh++;
+                }
+            }
+            if (hit) ca_next(CA, CAbeg[q] + CAlen[q], s.q[t], s.npos[t]);
+        }
+        if (!aev) {
+            s.UA += incA_of(crj);
+            s.UB += incB_of(crj);
+            const unsigned cnt = s.cntk - nh;
+            if (cnt) atomicAdd(g.acc + (size_t)b * C + ((s.cols >> (crj << 3)) & 0xffu), (unsigned long long)cnt);
+        }
+        j++;
+        if (anext < j) anext = next_a_event(codes, j, j1, lane);
     }
+    cross_flush<C, PART>(g, lut, H, cra, La, q0, nL, s, lane);
 }
 
-// item (k, jb): c = L_x[64k .. 64k+63], positions j in block jb of length kCrossBlock
+// item (k, jb): c = L_x[128k .. 128k+127], positions j in block jb of length kCrossBlock
 template <int C>
 __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint8_t *codes, const uint32_t *La, int nL,
                                            const uint32_t *CAbeg, const uint32_t *CAlen, const uint32_t *CA,
-                                           uint32_t cra, uint32_t a, uint32_t *H, const uint32_t *AP, int nap, int k,
-                                           int jb, int lane) {
+                                           uint32_t cra, uint32_t a, uint32_t *H, int k, int jb, int lane) {
     const int j0 = jb * kCrossBlock, j1 = min(D, j0 + kCrossBlock);
-    CrossC s0, s1;
-    cross_c_init(s0, La, nL, CAbeg, CAlen, CA, 64 * k + lane, j0);
-    cross_c_init(s1, La, nL, CAbeg, CAlen, CA, 64 * k + 32 + lane, j0);
-    unsigned M0 = 0, M1 = 0;
+    const int q0 = kStarW * k;
+    StarS s;
+    s.keys = 0;
 #pragma unroll
-    for (int q = 0; q < 3; q++) {
-        const unsigned m0 = __ballot_sync(kFull, s0.key == q), m1 = __ballot_sync(kFull, s1.key == q);
-        if (lane == q) { M0 = m0; M1 = m1; }
+    for (int t = 0; t < kStarM; t++) {
+        const int q = q0 + 32 * t + lane;
+        s.dA[t] = 0;
+        s.dB[t] = 0;
+        s.npos[t] = kInfPos;
+        s.q[t] = 0;
+        if (q < nL) {   // pointer to c's first R-neighbour at or after j0
+            const uint32_t q1 = CAbeg[q] + CAlen[q];
+            s.q[t] = CAbeg[q] - 1u;
+            do ca_next(CA, q1, s.q[t], s.npos[t]);
+            while (s.npos[t] < (uint32_t)j0);
+        }
     }
-    cross_span<C, 2>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, AP, nap, j0, min(j1, i), lane);
-    if (min(j1, i) > j0 && i + 1 < j1) {   // j = i is a's own position: skip the pointers past it
-        while (s0.npos <= (uint32_t)i) { s0.q++; cross_c_next(CA, s0); }
-        while (s1.npos <= (uint32_t)i) { s1.q++; cross_c_next(CA, s1); }
+    s.cntk = 0;
+#pragma unroll
+    for (uint32_t kk = 0; kk < 3; kk++) {
+        unsigned cnt = 0;
+#pragma unroll
+        for (int t = 0; t < kStarM; t++) {
+            const int q = q0 + 32 * t + lane;
+            cnt += __popc(__ballot_sync(kFull, q < nL && (La[q] & 3u) - 1u == kk));
+        }
+        if ((uint32_t)lane == kk) s.cntk = cnt;
     }
-    cross_span<C, 1>(g, lut, H, R, codes, CA, s0, s1, M0, M1, cra, AP, nap, max(j0, i + 1), j1, lane);
-    cross_c_flush<C>(g, s0, lut, H, cra);
-    cross_c_flush<C>(g, s1, lut, H, cra);
+    s.UA = 0;
+    s.UB = 0;
+    cross_part<C, 2>(g, lut, H, cra, R, codes, La, q0, nL, CAbeg, CAlen, CA, s, j0, min(j1, i), lane);
+    cross_part<C, 1>(g, lut, H, cra, R, codes, La, q0, nL, CAbeg, CAlen, CA, s, max(j0, i + 1), j1, lane);
     if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
     __syncwarp();
 }
@@ -1066,7 +999,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(g.skip & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
-        const int nck = (nL + 63) / 64, njb = (D + kCrossBlock - 1) / kCrossBlock;
+        const int nck = (nL + kStarW - 1) / kStarW, njb = (D + kCrossBlock - 1) / kCrossBlock;
         const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
         const int total = nch + nB + nL;
         // longest first across kinds: star chunks longer than a cross block, the "2+1" items,
@@ -1086,8 +1019,8 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             } else if (b_it >= 0) {
                 if (g.skip & 2) continue;
                 if (cross)
-                    cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, AP, nap,
-                                  b_it / njb, b_it % njb, lane);
+                    cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, b_it / njb,
+                                  b_it % njb, lane);
                 else
                     item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
                                        glist(g, R[i + 1 + b_it] >> 2), lane);
@@ -1172,9 +1105,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         uint32_t *lw = sm + L.light + wid * kLightWords;
         uint32_t *R = lw, *Las = lw + kLW, *Ba = lw + 2 * kLW, *Bb = Ba + kLB, *Bls = Bb + kLB;
         uint32_t *RS = Bls + kLB, *RO = RS + kSmax + 1, *LS = RO + kSmax, *LO = LS + kSmax + 1;
-        uint32_t *RL = LO + kSmax, *LL = RL + kLcap;   // staged adjacency lists
+        uint32_t *PL = LO + kSmax;   // staged adjacency lists: R's, then the current L_a's
         uint32_t *gw = g.glight + ((int64_t)blockIdx.x * kWarps + wid) * g.glight_per_warp;   // oversize L_a
-        Staged st{RL, RS, LL, LS, false, false};
+        Staged st{PL, RS, PL, LS, false, false};
         for (;;) {
             unsigned long long x = 0;
             if (lane == 0) x = atomicAdd(ctr + 1, 1ull);
@@ -1188,11 +1121,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int D = (int)(g.off[r + 1] - rs);
             for (int q = lane; q < D; q += 32) R[q] = g.adj[rs + q];
             __syncwarp();
-            st.rok = gather_lists(g, R, D, RS, RO, kSmax, RL, kLcap, lane);   // lists of R, once per root
+            st.rok = gather_lists(g, R, D, RS, RO, kSmax, PL, kPool, lane);   // lists of R, once per root
+            const int used = st.rok ? (int)RS[D] : 0;
+            uint32_t *LL = PL + used;
+            st.LL = LL;
             for (int64_t t = ta; t < tb; t++) {
                 const int i = (int)(t - t0);
                 const uint32_t a = R[i] >> 2;
-                const List al = list_at(g, R, i, RL, RS, st.rok);
+                const List al = list_at(g, R, i, PL, RS, st.rok);
                 uint32_t *La = Las, *Bl = Bls;
                 if (al.len > kLW) {   // only with a user-given order: lists longer than the smem slots
                     La = gw;
@@ -1201,7 +1137,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     __syncwarp();
                 }
                 const int nL = build_a(g, r, al, R, D, Ba, La, lane);
-                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kLcap, lane);
+                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
                 task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
                                  nullptr, -1, 0, lane);
                 flush_hist<C>(H, g.acc, r, a, lane);
