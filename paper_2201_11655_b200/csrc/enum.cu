@@ -47,6 +47,7 @@ constexpr int kBlock = kWarps * 32;
 constexpr int kLightDeg = 128;        // light root: G_U degree <= this (measured best of 64/128/256)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
+constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
 
 struct Dev {
     const int64_t *__restrict__ off;
@@ -57,7 +58,8 @@ struct Dev {
     const int32_t *__restrict__ heavy_task;   // task ids of heavy roots, rank order
     const int32_t *__restrict__ light_root;   // light roots, rank order
     int64_t nheavy, nlight;
-    unsigned long long *__restrict__ acc;     // [n][C], row = rank
+    unsigned long long *__restrict__ acc;     // accumulator, class-major: element (v = rank, col) at col * ns + v
+    uint32_t ns;                              // column stride = n
     uint32_t *__restrict__ gheavy;            // global fallback: per-CTA heavy buffers
     uint32_t *__restrict__ glight;            // global fallback: per-warp oversize L_a + bitmap
     int64_t gheavy_per_cta, glight_per_warp;  // words
@@ -66,7 +68,8 @@ struct Dev {
     int maxdeg;
     int off32;                                // n * C < 2^32: 32-bit accumulator offsets
     int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
-    int fold;                                 // star chunks: fold the 16-bit counters every this many b (<= 65535)
+    int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields)
+    int xblock;                               // cross items: positions per item (<= kMaxBlock)
     uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
     int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
     uint32_t ca_cap;
@@ -92,6 +95,14 @@ constexpr int kSmax = 64;                    // light: lists staged for at most 
 constexpr int kPool = 960;                   // light: staged list entries, R's lists then L_a's lists
 constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool;
 
+// accumulator element (v, col) at col * n + v.  Class-major: the updates of one class from many
+// sets share sectors with other vertices' updates of the same (hot) class, so a matrix far
+// larger than L2 still hits L2 for the few classes that dominate (cfg5: 417 -> 352 ms vs
+// row-major, profiles/r01_v8_*); rows are restored by k_finalize.
+__device__ __forceinline__ unsigned long long *accp(const Dev &g, uint32_t v, uint32_t col) {
+    return g.acc + ((size_t)col * g.ns + v);
+}
+
 __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x) {
     // position of vertex x in the sorted entry list S[0..len), or -1
     const uint32_t key = x << 2;
@@ -116,36 +127,33 @@ __device__ __forceinline__ void team_sync() {
 
 // one set with members r, a (histogram H), b (warp-uniform, merged per column) and c (lane)
 template <int C>
-__device__ __forceinline__ void emit4(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t b, uint32_t c,
-                                      int col, int lane) {
-    if (col != kNone) atomicAdd(acc + (size_t)c * C + col, 1ull);
+__device__ __forceinline__ void emit4(uint32_t *H, const Dev &g, uint32_t b, uint32_t c, int col, int lane) {
+    if (col != kNone) atomicAdd(accp(g, c, col), 1ull);
     const unsigned m = __match_any_sync(kFull, col);
     if (col != kNone && lane == __ffs(m) - 1) {
         const unsigned cnt = __popc(m);
-        H[col] += cnt;
-        atomicAdd(acc + (size_t)b * C + col, (unsigned long long)cnt);
+        atomicAdd(H + col, cnt);   // shared-memory reduction, result unused: no RMW dependency
+        atomicAdd(accp(g, b, col), (unsigned long long)cnt);
     }
 }
 
 // one set with members r, a (histogram H) and b (lane)
 template <int C>
-__device__ __forceinline__ void emit3(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t b, int col,
-                                      int lane) {
-    if (col != kNone) atomicAdd(acc + (size_t)b * C + col, 1ull);
+__device__ __forceinline__ void emit3(uint32_t *H, const Dev &g, uint32_t b, int col, int lane) {
+    if (col != kNone) atomicAdd(accp(g, b, col), 1ull);
     const unsigned m = __match_any_sync(kFull, col);
-    if (col != kNone && lane == __ffs(m) - 1) H[col] += __popc(m);
+    if (col != kNone && lane == __ffs(m) - 1) atomicAdd(H + col, (unsigned)__popc(m));
 }
 
 // warp-private histogram -> rows r and a
 template <int C>
-__device__ __forceinline__ void flush_hist(uint32_t *H, unsigned long long *__restrict__ acc, uint32_t r, uint32_t a,
-                                           int lane) {
+__device__ __forceinline__ void flush_hist(uint32_t *H, const Dev &g, uint32_t r, uint32_t a, int lane) {
     __syncwarp();
     for (int j = lane; j < C; j += 32) {
         const uint32_t v = H[j];
         if (v) {
-            atomicAdd(acc + (size_t)r * C + j, (unsigned long long)v);
-            atomicAdd(acc + (size_t)a * C + j, (unsigned long long)v);
+            atomicAdd(accp(g, r, j), (unsigned long long)v);
+            atomicAdd(accp(g, a, j), (unsigned long long)v);
             H[j] = 0;
         }
     }
@@ -351,8 +359,10 @@ __device__ void build_a_cta(const Dev &g, uint32_t r, List al, const uint32_t *R
 //     add it, in the class lut[key | code(r, b)], to b's row: one atomic per key present;
 //   * events (an a-b edge: every set of that b; a b-c edge: that c's set) are classified one
 //     by one through the LUT entry of their full mask (star_event).
-// Every set is counted once, in the class of its exact mask.  16-bit fields: U is folded into
-// the counts at least every g.fold iterations (65535).
+// Every set is counted once, in the class of its exact mask.  A work item is a chunk x a block
+// of at most g.fold (<= 65535: 16-bit fields) consecutive b positions: items of bounded length
+// balance a task's warps; at a block's end the c's still ahead take U and every c flushes.
+// Counts are packed in 10-bit fields (inc_of), so a block spans at most kMaxBlock = 1023 b's.
 constexpr int kStarM = 4;                  // c slots per lane
 constexpr int kStarW = 32 * kStarM;        // c positions per star chunk
 constexpr uint32_t kInfPos = 0x3fffffffu;
@@ -360,12 +370,14 @@ constexpr uint32_t kInfPos = 0x3fffffffu;
 // row offset of vertex v's column col in the accumulator (32-bit when n*C < 2^32)
 template <int C, bool OFF32>
 __device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, uint32_t col) {
-    if (OFF32) return g.acc + (v * (uint32_t)C + col);
-    return g.acc + ((size_t)v * C + col);
+    if (OFF32) return g.acc + (col * g.ns + v);
+    return g.acc + ((size_t)col * g.ns + v);
 }
 
-__device__ __forceinline__ uint32_t incA_of(uint32_t crb) { return crb == 1u ? 1u : (crb == 2u ? 0x10000u : 0u); }
-__device__ __forceinline__ uint32_t incB_of(uint32_t crb) { return crb == 3u ? 1u : 0u; }
+// one set in the 10-bit field of code(r, b) in {1, 2, 3}; a block spans <= 1023 b's, so no field
+// overflows, and packed corrections (U + d) are exact field by field (final fields in [0, 1023])
+__device__ __forceinline__ uint32_t inc_of(uint32_t crb) { return 1u << (crb * 10u - 10u); }
+constexpr int kMaxBlock = 1023;
 
 // c at position p: next entry of its induced list after index q with position < p, else INF
 __device__ __forceinline__ void nr_next(const Dev &g, int64_t seg, int p, uint32_t &q, uint32_t &npos) {
@@ -378,44 +390,27 @@ __device__ __forceinline__ void nr_next(const Dev &g, int64_t seg, int p, uint32
 }
 
 struct StarS {
-    uint32_t dA[kStarM], dB[kStarM];   // per c: count deltas, then (after its snapshot) its counts
+    uint32_t d[kStarM];                // per c: packed count deltas, then (after its snapshot) its counts
     uint32_t npos[kStarM], q[kStarM];  // next event position of c, index of that induced entry
     uint32_t keys;                     // 4 bits per slot: code(r,c) - 1 + 3 code(a,c); 15 = no c
-    uint32_t UA, UB;                   // warp-uniform plain counts: UA = n(crb=1) | n(crb=2) << 16, UB = n(crb=3)
+    uint32_t U;                        // warp-uniform plain counts, 10-bit fields: n(crb=1) | n(crb=2) << 10 | n(crb=3) << 20
     unsigned cntk;                     // key lanes: chunk c's after the current b with this lane's key
     uint32_t cols;                     // key lanes: column of (key | code(r,b)) in byte code(r,b)
 };
 
 template <int C>
 __device__ __forceinline__ void star_flush_c(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, uint32_t c,
-                                             uint32_t key, uint32_t fA, uint32_t fB) {
+                                             uint32_t key, uint32_t f) {
     const uint32_t lmask = cra | ((key % 3u) + 1u) << 4 | (key / 3u) << 8;
-    const uint32_t n[3] = {fA & 0xffffu, fA >> 16, fB};
+    const uint32_t n[3] = {f & 0x3ffu, (f >> 10) & 0x3ffu, f >> 20};
 #pragma unroll
     for (uint32_t crb = 1; crb <= 3; crb++) {
         if (n[crb - 1]) {
             const int col = lut[lmask | crb << 2];
-            atomicAdd(g.acc + (size_t)c * C + col, (unsigned long long)n[crb - 1]);
+            atomicAdd(accp(g, c, col), (unsigned long long)n[crb - 1]);
             atomicAdd(H + col, n[crb - 1]);
         }
     }
-}
-
-// fold: the live c's (p >= j) add U and flush their counts; U restarts (16-bit fields)
-template <int C>
-__device__ __forceinline__ void star_fold(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, const uint32_t *R,
-                                          StarS &s, int cb, int ce, int j, int lane) {
-#pragma unroll
-    for (int t = 0; t < kStarM; t++) {
-        const int p = cb + 32 * t + lane;
-        if (p < ce && p >= j) {
-            star_flush_c<C>(g, lut, H, cra, R[p] >> 2, (s.keys >> (4 * t)) & 15u, s.dA[t] + s.UA, s.dB[t] + s.UB);
-            s.dA[t] = 0;
-            s.dB[t] = 0;
-        }
-    }
-    s.UA = 0;
-    s.UB = 0;
 }
 
 // the c at position j (>= cb) takes its snapshot; its key lane stops counting it for b's
@@ -424,10 +419,7 @@ __device__ __forceinline__ void star_snapshot(StarS &s, int j, int cb, int lane)
 #pragma unroll
     for (int t = 0; t < kStarM; t++) {
         if (t == ts) {
-            if (lane == owner) {
-                s.dA[t] += s.UA;
-                s.dB[t] += s.UB;
-            }
+            if (lane == owner) s.d[t] += s.U;
             const uint32_t kk = __shfl_sync(kFull, (s.keys >> (4 * t)) & 15u, owner);
             if ((uint32_t)lane == kk) s.cntk--;
         }
@@ -457,15 +449,12 @@ __device__ __forceinline__ void star_event(const Dev &g, const uint8_t *lut, uin
             const uint32_t cbc = hit ? swap2(g.nr_adj[s.q[t]] & 3u) : 0u;   // the entry holds code(c, b)
             const uint32_t lmask = cra | ((key % 3u) + 1u) << 4 | (key / 3u) << 8;
             col = lut[lmask | crb << 2 | cab << 6 | cbc << 10];
-            atomicAdd(g.acc + (size_t)(R[p] >> 2) * C + col, 1ull);
+            atomicAdd(accp(g, R[p] >> 2, col), 1ull);
             atomicAdd(H + col, 1u);
-            if (!aev) {   // U will count this j for every c: take it back for this one
-                s.dA[t] -= incA_of(crb);
-                s.dB[t] -= incB_of(crb);
-            }
+            if (!aev) s.d[t] -= inc_of(crb);   // U will count this j for every c: take it back for this one
         }
         const unsigned m = __match_any_sync(kFull, col);
-        if (col != kNone && lane == __ffs(m) - 1) atomicAdd(g.acc + (size_t)b * C + col, (unsigned long long)__popc(m));
+        if (col != kNone && lane == __ffs(m) - 1) atomicAdd(accp(g, b, col), (unsigned long long)__popc(m));
         if (!aev) {
             for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
                 const uint32_t kk = __shfl_sync(kFull, key, __ffs(hm) - 1);
@@ -475,10 +464,9 @@ __device__ __forceinline__ void star_event(const Dev &g, const uint8_t *lut, uin
         if (hit) nr_next(g, seg, p, s.q[t], s.npos[t]);
     }
     if (!aev) {
-        s.UA += incA_of(crb);
-        s.UB += incB_of(crb);
+        s.U += inc_of(crb);
         const unsigned cnt = s.cntk - nh;
-        if (cnt) atomicAdd(g.acc + (size_t)b * C + ((s.cols >> (crb << 3)) & 0xffu), (unsigned long long)cnt);
+        if (cnt) atomicAdd(accp(g, b, ((s.cols >> (crb << 3)) & 0xffu)), (unsigned long long)cnt);
     }
 }
 
@@ -491,8 +479,7 @@ __device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarS
         for (int j = j0; j < j1; j++) {
             const uint32_t e = R[j];   // rank(b) << 2 | code(r, b)
             const uint32_t crb = e & 3u;
-            s.UA += incA_of(crb);
-            s.UB += incB_of(crb);
+            s.U += inc_of(crb);
             if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
                                   (unsigned long long)s.cntk);
         }
@@ -503,15 +490,11 @@ __device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarS
             const uint32_t kt = (s.keys >> (4 * t)) & 15u;
             for (int j = a0; j < a1; j++) {
                 const int owner = j - cb - 32 * t;
-                if (lane == owner) {
-                    s.dA[t] += s.UA;
-                    s.dB[t] += s.UB;
-                }
+                if (lane == owner) s.d[t] += s.U;
                 if ((uint32_t)lane == __shfl_sync(kFull, kt, owner)) s.cntk--;
                 const uint32_t e = R[j];
                 const uint32_t crb = e & 3u;
-                s.UA += incA_of(crb);
-                s.UB += incB_of(crb);
+                s.U += inc_of(crb);
                 if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
                                       (unsigned long long)s.cntk);
             }
@@ -544,30 +527,35 @@ __device__ __forceinline__ int next_a_event(const uint8_t *codes, int j, int jen
     return jend;
 }
 
-// chunk k of the task (r, a = R[i]): c positions [max(D - W(k+1), i+2), D - W k), the longest
-// chunks first
+// star item (k, jb) of the task (r, a = R[i]): c positions [cb, ce) = [max(D - W(k+1), i+2), D - W k)
+// (chunk k), b positions [jlo, jhi) = block jb of [i+1, ce) in steps of g.fold
+__device__ __forceinline__ int star_blocks(int D, int i, int k, int S) {
+    const int ce = D - kStarW * k;
+    return (ce - i - 1 + S - 1) / S;
+}
+
 template <int C>
-__device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
-                                           int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
-                                           uint32_t *H, int k, int lane) {
+__device__ __forceinline__ void star_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
+                                          int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
+                                          uint32_t *H, int k, int jb, int lane) {
     const int64_t seg = g.hbase[r];
     const int ce = D - kStarW * k, cb = max(ce - kStarW, i + 2);
+    const int jlo = i + 1 + jb * g.fold, jhi = min(ce, jlo + g.fold);
     StarS s;
     s.keys = 0;
 #pragma unroll
     for (int t = 0; t < kStarM; t++) {
         const int p = cb + 32 * t + lane;
-        s.dA[t] = 0;
-        s.dB[t] = 0;
+        s.d[t] = 0;
         s.npos[t] = kInfPos;
         s.q[t] = 0;
         uint32_t key = 15u;
-        if (p < ce) {
+        if (p < ce && p >= jlo) {   // c's before the block were completed by earlier blocks
             const uint32_t ec = R[p];
             key = (ec & 3u) - 1u + 3u * get2(Ba, p);
             s.q[t] = (uint32_t)g.nr_off[seg + p] - 1u;
-            do nr_next(g, seg, p, s.q[t], s.npos[t]);   // first induced neighbour after a
-            while (s.npos[t] <= (uint32_t)i);
+            do nr_next(g, seg, p, s.q[t], s.npos[t]);   // first induced neighbour in the block
+            while (s.npos[t] < (uint32_t)jlo);
         }
         s.keys |= key << (4 * t);
     }
@@ -585,35 +573,31 @@ __device__ __forceinline__ void star_chunk(const Dev &g, const uint8_t *lut, uin
         s.cols = (uint32_t)lut[kmask | 1u << 2] << 8 | (uint32_t)lut[kmask | 2u << 2] << 16 |
                  (uint32_t)lut[kmask | 3u << 2] << 24;
     }
-    s.UA = 0;
-    s.UB = 0;
-    int j = i + 1;
-    int anext = next_a_event(codes, j, ce, lane);
-    int jfold = j + g.fold;
-    while (j < ce) {
+    s.U = 0;
+    int j = jlo;
+    int anext = next_a_event(codes, j, jhi, lane);
+    while (j < jhi) {
         uint32_t cm = s.npos[0];
 #pragma unroll
         for (int t = 1; t < kStarM; t++) cm = min(cm, s.npos[t]);
         const int cev = (int)min(__reduce_min_sync(kFull, cm), kInfPos);
-        const int stop = min(min(ce, jfold), min(anext, cev));
+        const int stop = min(jhi, min(anext, cev));
         star_fast_any<C>(g, R, s, j, stop, cb, lane);
         j = stop;
-        if (j >= ce) break;
-        if (j == jfold) {
-            star_fold<C>(g, lut, H, cra, R, s, cb, ce, j, lane);
-            jfold = j + g.fold;
-            continue;
-        }
+        if (j >= jhi) break;
         star_event<C>(g, lut, H, cra, R, codes, seg, s, j, cb, ce, lane);
         j++;
-        if (anext < j) anext = next_a_event(codes, j, ce, lane);
+        if (anext < j) anext = next_a_event(codes, j, jhi, lane);
     }
 #pragma unroll
     for (int t = 0; t < kStarM; t++) {
         const int p = cb + 32 * t + lane;
-        if (p < ce) star_flush_c<C>(g, lut, H, cra, R[p] >> 2, (s.keys >> (4 * t)) & 15u, s.dA[t], s.dB[t]);
+        if (p < ce && p >= jlo) {
+            if (p >= jhi) s.d[t] += s.U;   // still ahead of the walk: every b of the block precedes it
+            star_flush_c<C>(g, lut, H, cra, R[p] >> 2, (s.keys >> (4 * t)) & 15u, s.d[t]);
+        }
     }
-    if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
+    if (g.big) flush_hist<C>(H, g, r, a, lane);
     __syncwarp();
 }
 
@@ -625,30 +609,46 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
                                             const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La, int nL,
                                             uint32_t *Bb, uint32_t *Bl, uint32_t *H, uint32_t cra, uint32_t a,
                                             List bl, int lane) {
-    unsigned long long *__restrict__ acc = g.acc;
     const uint32_t eb = R[j], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
-    for (int base = 0; base < bl.len; base += 32) {
-        const int p = base + lane;
-        int col = kNone;
-        uint32_t c = 0;
-        if (p < bl.len) {
-            const uint32_t e = bl.p[p];
-            c = e >> 2;
-            if (c > r) {
-                const int pos = find_rank(R, D, c);
-                if (pos >= 0) {
-                    if (NW == 1 && pos > j) set2(Bb, pos, e & 3u);
-                } else {
-                    const int q = find_rank(La, nL, c);
-                    if (q >= 0) set2(Bl, q, e & 3u);
-                    else col = lut[mb | (e & 3u) << 10];
+    bool tb = false, tl = false;   // this lane set a code in Bb / Bl
+    for (int base = 0; base < bl.len; base += 32 * kPF) {
+        uint32_t ev[kPF];   // kPF loads in flight per lane (b's list is often in global memory)
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+            const int p = base + 32 * u + lane;
+            ev[u] = p < bl.len ? bl.p[p] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+            if (base + 32 * u >= bl.len) break;
+            const uint32_t e = ev[u];
+            int col = kNone;
+            uint32_t c = 0;
+            if (base + 32 * u + lane < bl.len) {
+                c = e >> 2;
+                if (c > r) {
+                    const int pos = find_rank(R, D, c);
+                    if (pos >= 0) {
+                        if (NW == 1 && pos > j) {
+                            set2(Bb, pos, e & 3u);
+                            tb = true;
+                        }
+                    } else {
+                        const int q = find_rank(La, nL, c);
+                        if (q >= 0) {
+                            set2(Bl, q, e & 3u);
+                            tl = true;
+                        } else {
+                            col = lut[mb | (e & 3u) << 10];
+                        }
+                    }
                 }
             }
+            emit4<C>(H, g, b, c, col, lane);
         }
-        emit4<C>(H, acc, b, c, col, lane);
     }
-    __syncwarp();
+    const bool anyb = __any_sync(kFull, tb), anyl = __any_sync(kFull, tl);
     if constexpr (NW == 1) {   // "3": c in R after b
         for (int base = j + 1; base < D; base += 32) {
             const int p = base + lane;
@@ -659,7 +659,7 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
                 c = ec >> 2;
                 col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
             }
-            emit4<C>(H, acc, b, c, col, lane);
+            emit4<C>(H, g, b, c, col, lane);
         }
     }
     // "2+1": c in L_a
@@ -672,12 +672,12 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
             c = ec >> 2;
             col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
         }
-        emit4<C>(H, acc, b, c, col, lane);
+        emit4<C>(H, g, b, c, col, lane);
     }
     __syncwarp();
-    if (NW == 1) clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
-    clear_words(Bl, 0, (nL + 15) >> 4, lane);
-    if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    if (NW == 1 && anyb) clear_words(Bb, (j + 1) >> 4, (D + 15) >> 4, lane);
+    if (anyl) clear_words(Bl, 0, (nL + 15) >> 4, lane);
+    if (g.big) flush_hist<C>(H, g, r, a, lane);
     __syncwarp();
 }
 
@@ -687,28 +687,40 @@ template <int C>
 __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, uint32_t r, int x, const uint32_t *R,
                                              int D, const uint32_t *La, int nL, uint32_t *Bl, uint32_t *H,
                                              uint32_t cra, uint32_t a, List bl, int lane) {
-    unsigned long long *__restrict__ acc = g.acc;
     const uint32_t eb = La[x], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 6;
-    for (int base = 0; base < bl.len; base += 32) {
-        const int p = base + lane;
-        int col = kNone;
-        uint32_t c = 0;
-        if (p < bl.len) {
-            const uint32_t e = bl.p[p];
-            c = e >> 2;
-            if (c > r && find_rank(R, D, c) < 0) {
-                const int q = find_rank(La, nL, c);
-                if (q >= 0) {
-                    if (q > x) set2(Bl, q, e & 3u);
-                } else {
-                    col = lut[mb | (e & 3u) << 10];
+    bool tl = false;
+    for (int base = 0; base < bl.len; base += 32 * kPF) {
+        uint32_t ev[kPF];
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+            const int p = base + 32 * u + lane;
+            ev[u] = p < bl.len ? bl.p[p] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kPF; u++) {
+            if (base + 32 * u >= bl.len) break;
+            const uint32_t e = ev[u];
+            int col = kNone;
+            uint32_t c = 0;
+            if (base + 32 * u + lane < bl.len) {
+                c = e >> 2;
+                if (c > r && find_rank(R, D, c) < 0) {
+                    const int q = find_rank(La, nL, c);
+                    if (q >= 0) {
+                        if (q > x) {
+                            set2(Bl, q, e & 3u);
+                            tl = true;
+                        }
+                    } else {
+                        col = lut[mb | (e & 3u) << 10];
+                    }
                 }
             }
+            emit4<C>(H, g, b, c, col, lane);
         }
-        emit4<C>(H, acc, b, c, col, lane);
     }
-    __syncwarp();
+    const bool anyl = __any_sync(kFull, tl);
     for (int base = x + 1; base < nL; base += 32) {
         const int q = base + lane;
         int col = kNone;
@@ -718,11 +730,11 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
             c = ec >> 2;
             col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
         }
-        emit4<C>(H, acc, b, c, col, lane);
+        emit4<C>(H, g, b, c, col, lane);
     }
     __syncwarp();
-    clear_words(Bl, (x + 1) >> 4, (nL + 15) >> 4, lane);
-    if (g.big) flush_hist<C>(H, acc, r, a, lane);
+    if (anyl) clear_words(Bl, (x + 1) >> 4, (nL + 15) >> 4, lane);
+    if (g.big) flush_hist<C>(H, g, r, a, lane);
     __syncwarp();
 }
 
@@ -740,7 +752,7 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
 // U, corrected per c at its events; R[j] gets, from key lanes 0..2, the number of the chunk's
 // c's with that key; an x-R[j] edge makes every set of that j non-plain (classified alone), an
 // R[j]-c edge makes c's PART 1 set non-plain and removes its PART 2 set (c is in N(a)).
-constexpr int kCrossBlock = 1024;   // j-block length (< 2^16: the 16-bit count fields)
+constexpr int kCrossBlock = 512;    // default j-block length g.xblock (<= kMaxBlock: the 10-bit count fields)
 
 // c's R-neighbour list pointer: next entry (position of R, code(c, R[pos])) with position < jend
 __device__ __forceinline__ void ca_next(const uint32_t *CA, uint32_t q1, uint32_t &q, uint32_t &npos) {
@@ -756,22 +768,20 @@ __device__ __forceinline__ void cross_flush(const Dev &g, const uint8_t *lut, ui
         const int q = q0 + 32 * t + lane;
         if (q < nL) {
             const uint32_t ec = La[q], c = ec >> 2, cxc = ec & 3u;
-            const uint32_t fA = s.dA[t] + s.UA, fB = s.dB[t] + s.UB;
-            const uint32_t n[3] = {fA & 0xffffu, fA >> 16, fB};
+            const uint32_t f = s.d[t] + s.U;
+            const uint32_t n[3] = {f & 0x3ffu, (f >> 10) & 0x3ffu, f >> 20};
 #pragma unroll
             for (uint32_t crj = 1; crj <= 3; crj++) {
                 if (n[crj - 1]) {
                     const int col = PART == 1 ? lut[cra | crj << 2 | cxc << 8] : lut[crj | cra << 2 | cxc << 10];
-                    atomicAdd(g.acc + (size_t)c * C + col, (unsigned long long)n[crj - 1]);
+                    atomicAdd(accp(g, c, col), (unsigned long long)n[crj - 1]);
                     atomicAdd(H + col, n[crj - 1]);
                 }
             }
         }
-        s.dA[t] = 0;
-        s.dB[t] = 0;
+        s.d[t] = 0;
     }
-    s.UA = 0;
-    s.UB = 0;
+    s.U = 0;
 }
 
 // positions [j0, j1) of one part (all c's of the chunk valid throughout)
@@ -825,15 +835,12 @@ __device__ __forceinline__ void cross_part(const Dev &g, const uint8_t *lut, uin
                 } else {
                     col = lut[crj | cra << 2 | swap2(cxj) << 6 | cxc << 10];
                 }
-                atomicAdd(g.acc + (size_t)c * C + col, 1ull);
+                atomicAdd(accp(g, c, col), 1ull);
                 atomicAdd(H + col, 1u);
             }
-            if (hit && !aev) {   // U will count this j for every c: take it back for this one
-                s.dA[t] -= incA_of(crj);
-                s.dB[t] -= incB_of(crj);
-            }
+            if (hit && !aev) s.d[t] -= inc_of(crj);   // U will count this j for every c: take it back
             const unsigned m = __match_any_sync(kFull, col);
-            if (col != kNone && lane == __ffs(m) - 1) atomicAdd(g.acc + (size_t)b * C + col, (unsigned long long)__popc(m));
+            if (col != kNone && lane == __ffs(m) - 1) atomicAdd(accp(g, b, col), (unsigned long long)__popc(m));
             if (!aev) {
                 const uint32_t key = valid ? (La[q] & 3u) - 1u : 15u;
                 for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
@@ -844,10 +851,9 @@ __device__ __forceinline__ void cross_part(const Dev &g, const uint8_t *lut, uin
             if (hit) ca_next(CA, CAbeg[q] + CAlen[q], s.q[t], s.npos[t]);
         }
         if (!aev) {
-            s.UA += incA_of(crj);
-            s.UB += incB_of(crj);
+            s.U += inc_of(crj);
             const unsigned cnt = s.cntk - nh;
-            if (cnt) atomicAdd(g.acc + (size_t)b * C + ((s.cols >> (crj << 3)) & 0xffu), (unsigned long long)cnt);
+            if (cnt) atomicAdd(accp(g, b, ((s.cols >> (crj << 3)) & 0xffu)), (unsigned long long)cnt);
         }
         j++;
         if (anext < j) anext = next_a_event(codes, j, j1, lane);
@@ -861,15 +867,14 @@ __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uin
                                            int D, const uint8_t *codes, const uint32_t *La, int nL,
                                            const uint32_t *CAbeg, const uint32_t *CAlen, const uint32_t *CA,
                                            uint32_t cra, uint32_t a, uint32_t *H, int k, int jb, int lane) {
-    const int j0 = jb * kCrossBlock, j1 = min(D, j0 + kCrossBlock);
+    const int j0 = jb * g.xblock, j1 = min(D, j0 + g.xblock);
     const int q0 = kStarW * k;
     StarS s;
     s.keys = 0;
 #pragma unroll
     for (int t = 0; t < kStarM; t++) {
         const int q = q0 + 32 * t + lane;
-        s.dA[t] = 0;
-        s.dB[t] = 0;
+        s.d[t] = 0;
         s.npos[t] = kInfPos;
         s.q[t] = 0;
         if (q < nL) {   // pointer to c's first R-neighbour at or after j0
@@ -890,11 +895,10 @@ __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uin
         }
         if ((uint32_t)lane == kk) s.cntk = cnt;
     }
-    s.UA = 0;
-    s.UB = 0;
+    s.U = 0;
     cross_part<C, 2>(g, lut, H, cra, R, codes, La, q0, nL, CAbeg, CAlen, CA, s, j0, min(j1, i), lane);
     cross_part<C, 1>(g, lut, H, cra, R, codes, La, q0, nL, CAbeg, CAlen, CA, s, max(j0, i + 1), j1, lane);
-    if (g.big) flush_hist<C>(H, g.acc, r, a, lane);
+    if (g.big) flush_hist<C>(H, g, r, a, lane);
     __syncwarp();
 }
 
@@ -905,7 +909,11 @@ template <int NW>
 __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const uint32_t *R, int D,
                                          const uint32_t *La, int nL, uint32_t *CAbeg, uint32_t *CAlen, uint32_t *CA,
                                          int *s_ca, int w, int lane) {
-    for (int q = w; q < nL; q += NW) {
+    for (;;) {   // c's taken from a shared counter (s_ca[1]): a hub c's long list does not stall one warp's share
+        int q = 0;
+        if (lane == 0) q = atomicAdd(s_ca + 1, 1);
+        q = __shfl_sync(kFull, q, 0);
+        if (q >= nL) break;
         const uint32_t c = La[q] >> 2;
         const int64_t c0 = g.off[c], c1 = g.off[c + 1];
         int cnt = 0;
@@ -960,7 +968,6 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
                                            int *s_ca, const Staged *st, const uint32_t *AP, int nap, int w,
                                            int lane) {
-    unsigned long long *__restrict__ acc = g.acc;
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -973,7 +980,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                 b = eb >> 2;
                 col = lut[cra | (eb & 3u) << 2 | get2(Ba, p) << 4];
             }
-            emit3<C>(H, acc, b, col, lane);
+            emit3<C>(H, g, b, col, lane);
         }
         // "1+1": b in L_a.   (r,b) = 0
         for (int base = w * 32; base < nL; base += NW * 32) {
@@ -985,9 +992,9 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                 b = eb >> 2;
                 col = lut[cra | (eb & 3u) << 4];
             }
-            emit3<C>(H, acc, b, col, lane);
+            emit3<C>(H, g, b, col, lane);
         }
-        if (g.big) flush_hist<C>(H, acc, r, a, lane);
+        if (g.big) flush_hist<C>(H, g, r, a, lane);
     } else if constexpr (NW == 1) {
         for (int j = i + 1; !(g.skip & 2) && j < D; j++)
             item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a,
@@ -999,23 +1006,32 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(g.skip & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
-        const int nck = (nL + kStarW - 1) / kStarW, njb = (D + kCrossBlock - 1) / kCrossBlock;
+        int nstar = 0;   // star items: chunk x block of b positions
+        for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, g.fold);
+        const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
         const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
-        const int total = nch + nB + nL;
-        // longest first across kinds: star chunks longer than a cross block, the "2+1" items,
-        // the remaining star chunks, then the b-in-L_a items
-        const int nlong = cross ? max(0, min(nch, (D - i - 2 - kCrossBlock) / kStarW + 1)) : nch;
+        const int total = nstar + nB + nL;
+        // star items (bounded length), then the "2+1" items, then the b-in-L_a items
         for (;;) {
             int it = 0;
             if (lane == 0) it = atomicAdd(wctr, 1);
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
-            int star_k = -1, b_it = -1;
-            if (it < nlong) star_k = it;
-            else if (it < nlong + nB) b_it = it - nlong;
-            else if (it < nch + nB) star_k = it - nB;
+            int star_k = -1, star_b = 0, b_it = -1;
+            if (it < nstar) {
+                int rem = it, kk = 0;
+                for (;; kk++) {
+                    const int nb = star_blocks(D, i, kk, g.fold);
+                    if (rem < nb) break;
+                    rem -= nb;
+                }
+                star_k = kk;
+                star_b = rem;
+            } else if (it < nstar + nB) {
+                b_it = it - nstar;
+            }
             if (star_k >= 0) {
-                if (!(g.skip & 1)) star_chunk<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, lane);
+                if (!(g.skip & 1)) star_item<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, star_b, lane);
             } else if (b_it >= 0) {
                 if (g.skip & 2) continue;
                 if (cross)
@@ -1026,8 +1042,8 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                                        glist(g, R[i + 1 + b_it] >> 2), lane);
             } else {
                 if (!(g.skip & 4))
-                    item_b_in_La<C>(g, lut, r, it - nch - nB, R, D, La, nL, Bl, H, cra, a,
-                                    glist(g, La[it - nch - nB] >> 2), lane);
+                    item_b_in_La<C>(g, lut, r, it - nstar - nB, R, D, La, nL, Bl, H, cra, a,
+                                    glist(g, La[it - nstar - nB] >> 2), lane);
             }
         }
     }
@@ -1040,7 +1056,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item;
-    __shared__ int s_nL, s_work, s_ca, s_nap;
+    __shared__ int s_nL, s_work, s_ca[2], s_nap;   // s_ca: CA space used, next c of ca_build
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
@@ -1082,15 +1098,16 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             for (int q = tid; q < 4 * ((al.len + 31) >> 5); q += kBlock) hb[L.Bl + q] = 0;   // build_a_cta scratch
             if (tid == 0) {
                 s_work = 0;
-                s_ca = 0;
+                s_ca[0] = 0;
+                s_ca[1] = 0;
             }
             if (K == 4)   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2
                 for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, &s_ca, nullptr, AP,
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, AP,
                                   s_nap <= kAPcap ? s_nap : -1, wid, lane);
-            flush_hist<C>(H, g.acc, r, R[i] >> 2, lane);
+            flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
             __syncthreads();
@@ -1140,7 +1157,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
                 task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
                                  nullptr, -1, 0, lane);
-                flush_hist<C>(H, g.acc, r, a, lane);
+                flush_hist<C>(H, g, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
             }
@@ -1149,14 +1166,27 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
 }
 
 // S9: rows from rank order to original ids
+// S9: acc is class-major [C][n] (rank order); out is row-major [original id][C].  A CTA
+// transposes a tile of kFinV consecutive ranks through shared memory: reads of acc[j][v0..)
+// and writes of each output row are both contiguous.
+constexpr int kFinV = 16;
 template <int C>
-__global__ void k_finalize(int64_t n, const int32_t *__restrict__ order, const unsigned long long *__restrict__ acc,
-                           unsigned long long *__restrict__ out) {
-    const int64_t total = n * C;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = idx / C, j = idx - v * C;
-        out[(int64_t)order[v] * C + j] = acc[idx];
+__global__ void __launch_bounds__(256) k_finalize(int64_t n, const int32_t *__restrict__ order,
+                                                  const unsigned long long *__restrict__ acc,
+                                                  unsigned long long *__restrict__ out) {
+    __shared__ unsigned long long tile[kFinV][C + 1];
+    for (int64_t v0 = (int64_t)blockIdx.x * kFinV; v0 < n; v0 += (int64_t)gridDim.x * kFinV) {
+        const int nv = (int)(n - v0 < kFinV ? n - v0 : kFinV);
+        for (int idx = threadIdx.x; idx < kFinV * C; idx += blockDim.x) {
+            const int j = idx / kFinV, vi = idx - j * kFinV;
+            if (vi < nv) tile[vi][j] = acc[(int64_t)j * n + v0 + vi];
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < nv * C; idx += blockDim.x) {
+            const int vi = idx / C, j = idx - vi * C;
+            out[(int64_t)order[v0 + vi] * C + j] = tile[vi][j];
+        }
+        __syncthreads();
     }
 }
 
@@ -1493,11 +1523,16 @@ static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int6
     if (const char *sk = getenv("VDMC_SKIP")) {   // profiling only; results incomplete
         d.skip = atoi(sk);
     }
-    d.fold = 65535;
+    d.fold = kMaxBlock;
+    d.xblock = kCrossBlock;
+    if (const char *xb = getenv("VDMC_XBLOCK")) {   // tuning: cross-item block length
+        d.xblock = std::max(32, std::min(kMaxBlock, atoi(xb)));
+    }
     if (const char *fo = getenv("VDMC_FOLD")) {   // tests: exercise the fold path on small graphs
-        d.fold = std::max(1, std::min(65535, atoi(fo)));
+        d.fold = std::max(1, std::min(kMaxBlock, atoi(fo)));
     }
     d.acc = (unsigned long long *)g->acc;
+    d.ns = (uint32_t)std::max<int64_t>(g->n, 1);
     d.gheavy = g->lscratch;
     d.glight = g->lscratch + (size_t)grid * per_cta;
     d.gca = g->lscratch + (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
@@ -1518,8 +1553,7 @@ static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int6
     }
     if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[2], s));
     if (g->n > 0) {
-        const int64_t total = g->n * C;
-        const unsigned fg = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)nsm * 16);
+        const unsigned fg = (unsigned)std::min<int64_t>((g->n + kFinV - 1) / kFinV, (int64_t)nsm * 8);
         k_finalize<C><<<fg, 256, 0, s>>>(g->n, g->order, (const unsigned long long *)g->acc,
                                            (unsigned long long *)counts);
         VDMC_LAUNCH();

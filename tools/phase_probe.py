@@ -21,9 +21,13 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("heavy, skip b in L_a", {"VDMC_PHASES": "1", "VDMC_SKIP": "4"}),
             ("heavy, skip all", {"VDMC_PHASES": "1", "VDMC_SKIP": "7"}),
             ("no cross items (fallback)", {"VDMC_SKIP": "8"}),
-            ("heavy, skip all, no ca_build", {"VDMC_PHASES": "1", "VDMC_SKIP": "15"})]
+            ("heavy, skip all, no ca_build", {"VDMC_PHASES": "1", "VDMC_SKIP": "15"}),
+            ("xblock 256", {"VDMC_XBLOCK": "256"}),
+            ("xblock 1023", {"VDMC_XBLOCK": "1023"}),
+            ("star block 512", {"VDMC_FOLD": "512"}), ("star block 256", {"VDMC_FOLD": "256"}),
+            ("star 512 xblock 256", {"VDMC_FOLD": "512", "VDMC_XBLOCK": "256"})]
 for label, env in variants:
-    for key in ("VDMC_PHASES", "VDMC_SKIP"):
+    for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_XBLOCK", "VDMC_FOLD"):
         os.environ.pop(key, None)
     os.environ.update(env)
     ts = []
