@@ -92,8 +92,9 @@ constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 // per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
 constexpr int kAPcap = 1024;                 // heavy: positions of R adjacent to a, kept for the fast loops
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
-constexpr int kPool = 960;                   // light: staged list entries, R's lists then L_a's lists
-constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool;
+constexpr int kPool = 896;                   // light: staged list entries, R's lists then L_a's lists
+constexpr int kFW = 32;                      // light: 1024-bit membership filters of R and of L_a
+constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool + 2 * kFW;
 
 // accumulator element (v, col) at col * n + v.  Class-major: the updates of one class from many
 // sets share sectors with other vertices' updates of the same (hot) class, so a matrix far
@@ -101,6 +102,20 @@ constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool;
 // row-major, profiles/r01_v8_*); rows are restored by k_finalize.
 __device__ __forceinline__ unsigned long long *accp(const Dev &g, uint32_t v, uint32_t col) {
     return g.acc + ((size_t)col * g.ns + v);
+}
+
+// Light walks: a 1024-bit one-hash filter of a vertex set (R per root, L_a per task).  A clear
+// bit proves the vertex is not in the set, so most list entries skip the binary search (in ER
+// graphs nearly every walked entry is in neither); a set bit falls back to the exact search.
+__device__ __forceinline__ uint32_t fhash(uint32_t v) { return (v * 0x9E3779B1u) >> 22; }
+__device__ __forceinline__ bool fmay(const uint32_t *F, uint32_t v) {
+    if (!F) return true;
+    const uint32_t h = fhash(v);
+    return (F[h >> 5] >> (h & 31u)) & 1u;
+}
+__device__ __forceinline__ void fadd(uint32_t *F, uint32_t v) {
+    const uint32_t h = fhash(v);
+    atomicOr(F + (h >> 5), 1u << (h & 31u));
 }
 
 __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x) {
@@ -186,12 +201,15 @@ __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S
         const int q = b0 + lane;
         int len = 0;
         uint32_t o = 0;
+        bool big = false;
         if (q < m) {
             const uint32_t v = V[q] >> 2;
             const int64_t x0 = g.off[v];
             o = (uint32_t)x0;
+            big = x0 > 0xffffffffll;   // 32-bit staged offsets: graphs past 2^32 entries are not staged
             len = (int)(g.off[v + 1] - x0);
         }
+        if (__any_sync(kFull, big)) return false;
         int inc = len;   // inclusive warp scan
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -208,6 +226,8 @@ __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S
     if (total > cap) return false;
     if (lane == 0) S[m] = (uint32_t)total;
     __syncwarp();
+    // asynchronous global -> shared copies (cp.async): every entry of the gather is in flight at
+    // once instead of one dependent load per lane and step
 #pragma unroll 4
     for (int f = lane; f < total; f += 32) {
         int lo = 0, hi = m;   // last q with S[q] <= f
@@ -216,8 +236,12 @@ __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S
             if ((int)S[mid] <= f) lo = mid;
             else hi = mid;
         }
-        B[f] = g.adj[(int64_t)O[lo] + (f - (int)S[lo])];
+        const uint32_t *src = g.adj + ((int64_t)O[lo] + (f - (int)S[lo]));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(B + f)),
+                     "l"(src)
+                     : "memory");
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
     return true;
 }
@@ -227,6 +251,7 @@ struct Staged {
     const uint32_t *RL, *RS;   // lists of the vertices of R     (valid if rok)
     const uint32_t *LL, *LS;   // lists of the vertices of L_a   (valid if lok)
     bool rok, lok;
+    const uint32_t *FR, *FL;   // membership filters of R and L_a
 };
 __device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, const uint32_t *B, const uint32_t *S,
                                         bool ok) {
@@ -237,7 +262,7 @@ __device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, 
 // Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
 // al = a's list.  Run by one warp.  Returns |L_a|.
 __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
-                       int lane, uint32_t *AP = nullptr, int *nap = nullptr) {
+                       int lane, uint32_t *AP = nullptr, int *nap = nullptr, const uint32_t *FR = nullptr) {
     // AP (optional): the positions of R adjacent to a, ascending (*nap = their number)
     int nL = 0, nA = 0;
     for (int base = 0; base < al.len; base += 32) {
@@ -249,7 +274,7 @@ __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int
             e = al.p[p];
             const uint32_t x = e >> 2;
             if (x > r) {
-                pos = find_rank(R, D, x);
+                pos = fmay(FR, x) ? find_rank(R, D, x) : -1;
                 if (pos >= 0) set2(Ba, pos, e & 3u);
                 else keep = true;
             }
@@ -608,7 +633,8 @@ template <int C, int NW>
 __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, uint32_t r, int i, int j,
                                             const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La, int nL,
                                             uint32_t *Bb, uint32_t *Bl, uint32_t *H, uint32_t cra, uint32_t a,
-                                            List bl, int lane) {
+                                            List bl, int lane, const uint32_t *FR = nullptr,
+                                            const uint32_t *FL = nullptr) {
     const uint32_t eb = R[j], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 2 | get2(Ba, j) << 6;
     bool tb = false, tl = false;   // this lane set a code in Bb / Bl
@@ -628,14 +654,14 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
             if (base + 32 * u + lane < bl.len) {
                 c = e >> 2;
                 if (c > r) {
-                    const int pos = find_rank(R, D, c);
+                    const int pos = fmay(FR, c) ? find_rank(R, D, c) : -1;
                     if (pos >= 0) {
                         if (NW == 1 && pos > j) {
                             set2(Bb, pos, e & 3u);
                             tb = true;
                         }
                     } else {
-                        const int q = find_rank(La, nL, c);
+                        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
                         if (q >= 0) {
                             set2(Bl, q, e & 3u);
                             tl = true;
@@ -686,7 +712,8 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
 template <int C>
 __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, uint32_t r, int x, const uint32_t *R,
                                              int D, const uint32_t *La, int nL, uint32_t *Bl, uint32_t *H,
-                                             uint32_t cra, uint32_t a, List bl, int lane) {
+                                             uint32_t cra, uint32_t a, List bl, int lane, const uint32_t *FR = nullptr,
+                                             const uint32_t *FL = nullptr) {
     const uint32_t eb = La[x], b = eb >> 2;
     const uint32_t mb = cra | (eb & 3u) << 6;
     bool tl = false;
@@ -705,8 +732,8 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
             uint32_t c = 0;
             if (base + 32 * u + lane < bl.len) {
                 c = e >> 2;
-                if (c > r && find_rank(R, D, c) < 0) {
-                    const int q = find_rank(La, nL, c);
+                if (c > r && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
+                    const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
                     if (q >= 0) {
                         if (q > x) {
                             set2(Bl, q, e & 3u);
@@ -998,10 +1025,10 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
     } else if constexpr (NW == 1) {
         for (int j = i + 1; !(g.skip & 2) && j < D; j++)
             item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a,
-                              list_at(g, R, j, st->RL, st->RS, st->rok), lane);
+                              list_at(g, R, j, st->RL, st->RS, st->rok), lane, st->FR, st->FL);
         for (int x = 0; !(g.skip & 4) && x < nL; x++)
             item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, list_at(g, La, x, st->LL, st->LS, st->lok),
-                            lane);
+                            lane, st->FR, st->FL);
     } else {
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(g.skip & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
@@ -1123,8 +1150,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         uint32_t *R = lw, *Las = lw + kLW, *Ba = lw + 2 * kLW, *Bb = Ba + kLB, *Bls = Bb + kLB;
         uint32_t *RS = Bls + kLB, *RO = RS + kSmax + 1, *LS = RO + kSmax, *LO = LS + kSmax + 1;
         uint32_t *PL = LO + kSmax;   // staged adjacency lists: R's, then the current L_a's
+        uint32_t *FR = PL + kPool, *FL = FR + kFW;
         uint32_t *gw = g.glight + ((int64_t)blockIdx.x * kWarps + wid) * g.glight_per_warp;   // oversize L_a
-        Staged st{PL, RS, PL, LS, false, false};
+        Staged st{PL, RS, PL, LS, false, false, FR, FL};
         for (;;) {
             unsigned long long x = 0;
             if (lane == 0) x = atomicAdd(ctr + 1, 1ull);
@@ -1136,7 +1164,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             if (ta >= tb) continue;
             const int64_t rs = g.split[r];
             const int D = (int)(g.off[r + 1] - rs);
-            for (int q = lane; q < D; q += 32) R[q] = g.adj[rs + q];
+            FR[lane] = 0;
+            __syncwarp();
+            for (int q = lane; q < D; q += 32) {
+                const uint32_t e = g.adj[rs + q];
+                R[q] = e;
+                fadd(FR, e >> 2);
+            }
             __syncwarp();
             st.rok = gather_lists(g, R, D, RS, RO, kSmax, PL, kPool, lane);   // lists of R, once per root
             const int used = st.rok ? (int)RS[D] : 0;
@@ -1153,7 +1187,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     clear_words(Bl, 0, (al.len + 15) >> 4, lane);
                     __syncwarp();
                 }
-                const int nL = build_a(g, r, al, R, D, Ba, La, lane);
+                const int nL = build_a(g, r, al, R, D, Ba, La, lane, nullptr, nullptr, FR);
+                FL[lane] = 0;
+                __syncwarp();
+                for (int q = lane; q < nL; q += 32) fadd(FL, La[q] >> 2);
+                __syncwarp();
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
                 task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
                                  nullptr, -1, 0, lane);

@@ -1,5 +1,5 @@
 """Time k_enum with phases / loop kinds switched off (profiling only, results incomplete):
-python tools/phase_probe.py cfg4 [k]"""
+python tools/phase_probe.py cfg4 [k] [quick]"""
 import os
 import sys
 
@@ -26,6 +26,8 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("xblock 1023", {"VDMC_XBLOCK": "1023"}),
             ("star block 512", {"VDMC_FOLD": "512"}), ("star block 256", {"VDMC_FOLD": "256"}),
             ("star 512 xblock 256", {"VDMC_FOLD": "512", "VDMC_XBLOCK": "256"})]
+if len(sys.argv) > 3 and sys.argv[3] == "quick":
+    variants = variants[:3]
 for label, env in variants:
     for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_XBLOCK", "VDMC_FOLD"):
         os.environ.pop(key, None)
