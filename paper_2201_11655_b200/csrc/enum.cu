@@ -399,6 +399,14 @@ __device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, 
     return g.acc + ((size_t)col * g.ns + v);
 }
 
+// predicated fire-and-forget u64 add (no divergent branch around it in the uniform b loops)
+__device__ __forceinline__ void red_if(bool p, unsigned long long *addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u64 [%0], %1;\n\t}\n" ::"l"(addr),
+        "l"((unsigned long long)v), "r"((uint32_t)p)
+        : "memory");
+}
+
 // one set in the 10-bit field of code(r, b) in {1, 2, 3}; a block spans <= 1023 b's, so no field
 // overflows, and packed corrections (U + d) are exact field by field (final fields in [0, 1023])
 __device__ __forceinline__ uint32_t inc_of(uint32_t crb) { return 1u << (crb * 10u - 10u); }
@@ -505,8 +513,7 @@ __device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarS
             const uint32_t e = R[j];   // rank(b) << 2 | code(r, b)
             const uint32_t crb = e & 3u;
             s.U += inc_of(crb);
-            if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
-                                  (unsigned long long)s.cntk);
+            red_if(s.cntk != 0u, acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu), s.cntk);
         }
     } else {
 #pragma unroll
@@ -520,8 +527,7 @@ __device__ __forceinline__ void star_fast(const Dev &g, const uint32_t *R, StarS
                 const uint32_t e = R[j];
                 const uint32_t crb = e & 3u;
                 s.U += inc_of(crb);
-                if (s.cntk) atomicAdd(acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu),
-                                      (unsigned long long)s.cntk);
+                red_if(s.cntk != 0u, acc_at<C, OFF32>(g, e >> 2, (s.cols >> (crb << 3)) & 0xffu), s.cntk);
             }
         }
     }
