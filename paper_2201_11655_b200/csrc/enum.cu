@@ -140,24 +140,44 @@ __device__ __forceinline__ void team_sync() {
     else __syncthreads();
 }
 
+// predicated fire-and-forget u64 add (no divergent branch around it in the uniform b loops)
+__device__ __forceinline__ void red_if(bool p, unsigned long long *addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u64 [%0], %1;\n\t}\n" ::"l"(addr),
+        "l"((unsigned long long)v), "r"((uint32_t)p)
+        : "memory");
+}
+
+// predicated shared-memory u32 reduction (histograms)
+__device__ __forceinline__ void red_shared_if(bool p, uint32_t *addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.add.u32 [%0], %1;\n\t}\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(addr)),
+        "r"(v), "r"((uint32_t)p)
+        : "memory");
+}
+
 // one set with members r, a (histogram H), b (warp-uniform, merged per column) and c (lane)
 template <int C>
 __device__ __forceinline__ void emit4(uint32_t *H, const Dev &g, uint32_t b, uint32_t c, int col, int lane) {
-    if (col != kNone) atomicAdd(accp(g, c, col), 1ull);
+    const bool v = col != kNone;
+    const uint32_t cc = v ? (uint32_t)col : 0u;
+    red_if(v, accp(g, c, cc), 1u);
     const unsigned m = __match_any_sync(kFull, col);
-    if (col != kNone && lane == __ffs(m) - 1) {
-        const unsigned cnt = __popc(m);
-        atomicAdd(H + col, cnt);   // shared-memory reduction, result unused: no RMW dependency
-        atomicAdd(accp(g, b, col), (unsigned long long)cnt);
-    }
+    const bool lead = v && lane == __ffs(m) - 1;   // one lane per distinct column (predicated, no branch)
+    const uint32_t cnt = __popc(m);
+    red_shared_if(lead, H + cc, cnt);
+    red_if(lead, accp(g, b, cc), cnt);
 }
 
 // one set with members r, a (histogram H) and b (lane)
 template <int C>
 __device__ __forceinline__ void emit3(uint32_t *H, const Dev &g, uint32_t b, int col, int lane) {
-    if (col != kNone) atomicAdd(accp(g, b, col), 1ull);
+    const bool v = col != kNone;
+    const uint32_t cc = v ? (uint32_t)col : 0u;
+    red_if(v, accp(g, b, cc), 1u);
     const unsigned m = __match_any_sync(kFull, col);
-    if (col != kNone && lane == __ffs(m) - 1) atomicAdd(H + col, (unsigned)__popc(m));
+    red_shared_if(v && lane == __ffs(m) - 1, H + cc, (uint32_t)__popc(m));
 }
 
 // warp-private histogram -> rows r and a
@@ -399,13 +419,6 @@ __device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, 
     return g.acc + ((size_t)col * g.ns + v);
 }
 
-// predicated fire-and-forget u64 add (no divergent branch around it in the uniform b loops)
-__device__ __forceinline__ void red_if(bool p, unsigned long long *addr, uint32_t v) {
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u64 [%0], %1;\n\t}\n" ::"l"(addr),
-        "l"((unsigned long long)v), "r"((uint32_t)p)
-        : "memory");
-}
 
 // one set in the 10-bit field of code(r, b) in {1, 2, 3}; a block spans <= 1023 b's, so no field
 // overflows, and packed corrections (U + d) are exact field by field (final fields in [0, 1023])
