@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvdmc.so")
+LIB_PATH = os.environ.get("VDMC_LIB") or os.path.join(_HERE, "lib", "libvdmc.so")   # VDMC_LIB: A/B builds
 
 VDMC_OK = 0
 STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASYM",
