@@ -694,25 +694,20 @@ __device__ __forceinline__ void item_b_in_R(const Dev &g, const uint8_t *lut, ui
         }
     }
     const bool anyb = __any_sync(kFull, tb), anyl = __any_sync(kFull, tl);
-    if constexpr (NW == 1) {   // "3": c in R after b
-        for (int base = j + 1; base < D; base += 32) {
-            const int p = base + lane;
-            int col = kNone;
-            uint32_t c = 0;
-            if (p < D) {
-                const uint32_t ec = R[p];
-                c = ec >> 2;
-                col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
-            }
-            emit4<C>(H, g, b, c, col, lane);
-        }
-    }
-    // "2+1": c in L_a
-    for (int base = 0; base < nL; base += 32) {
-        const int q = base + lane;
+    // "3" (c in R after b; light tasks) and "2+1" (c in L_a) in one index space, so a warp
+    // iteration is filled from both when they are short
+    const int n3 = NW == 1 ? D - j - 1 : 0;
+    for (int base = 0; base < n3 + nL; base += 32) {
+        const int x = base + lane;
         int col = kNone;
         uint32_t c = 0;
-        if (q < nL) {
+        if (x < n3) {
+            const int p = j + 1 + x;
+            const uint32_t ec = R[p];
+            c = ec >> 2;
+            col = lut[mb | (ec & 3u) << 4 | get2(Ba, p) << 8 | get2(Bb, p) << 10];
+        } else if (x < n3 + nL) {
+            const int q = x - n3;
             const uint32_t ec = La[q];
             c = ec >> 2;
             col = lut[mb | (ec & 3u) << 8 | get2(Bl, q) << 10];
