@@ -99,8 +99,9 @@ vdmc_status vdmc_build_graph(int64_t n, const int64_t *indptr, const int32_t *nb
  * original vertex id, fully overwritten.  work = NULL counts everything; otherwise only the
  * motifs whose (root, depth-1 neighbour) task lies in *work.  The partials of any set of
  * disjoint slices covering [0, ntasks) sum to the full result bit-exactly (integer adds).
- * Asynchronous on `stream`; valid after the stream synchronises.
- * Errors: VDMC_EK, VDMC_EINVAL (NULL, bad slice), VDMC_ENOMEM, VDMC_ECUDA. */
+ * Asynchronous on `stream`; valid after the stream synchronises.  The call itself may
+ * synchronise `stream` once per graph (first count: schedule lists and the heavy-root pre-pass).
+ * Errors: VDMC_EK, VDMC_EINVAL (NULL, bad slice, G_U degree >= 2^21), VDMC_ENOMEM, VDMC_ECUDA. */
 vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
                        void *stream);
 
