@@ -232,3 +232,26 @@ def test_block_cache_reuse_and_trim(vd, oracle_mod):
         for g, w in zip(gs, want):
             assert np.array_equal(gpu_count(vd, g, 4), w)
         vd.trim(torch.cuda.current_device())
+
+
+def test_64bit_accumulator_offsets(vd, oracle_mod):
+    """n x C >= 2^32 (n = 22M, C = 199): the accumulator's class-major offsets col * n + v pass
+    2^32, so the 64-bit addressing path runs (off32 = 0).  A small random graph placed on
+    scattered ids among 22M otherwise isolated vertices must give the oracle's rows; every
+    other row is zero."""
+    import torch
+    n = 22_000_000
+    assert n * vd.num_classes(4) >= 2 ** 32
+    small = G.random_small(30, 0.25, 77)
+    ids = np.sort(np.random.default_rng(5).choice(n, 30, replace=False)).astype(np.int32)
+    s = torch.from_numpy(ids[small[1]]).cuda()
+    d = torch.from_numpy(ids[small[2]]).cuda()
+    gr = vd.Graph(n, s, d)
+    for k in (3, 4):
+        out = gr.count(k)
+        rows = out[torch.from_numpy(ids).long().cuda()].cpu().numpy().view(np.uint64)
+        assert np.array_equal(rows, oracle_mod.count_brute(small, k))
+        assert int(out.sum().item()) == int(rows.astype(np.int64).sum())
+        del out
+    gr.close()
+    vd.trim(torch.cuda.current_device())
