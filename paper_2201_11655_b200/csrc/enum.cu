@@ -82,7 +82,6 @@ struct Dev {
 struct Layout {
     int R, La, Ba, Bb, Bl;        // heavy: R[maxdeg], La[maxdeg], Ba[bw], Bb[kWarps][bw], Bl[kWarps][lw]
     int bw, lw;                   // bitmap words for R positions / L positions
-    int AP;                       // heavy: positions of R adjacent to a [kAPcap]
     int hist;                     // per-warp u32 histograms [kWarps][C]
     int light;                    // light region: per warp kLightWords
     int total;                    // words
@@ -90,7 +89,6 @@ struct Layout {
 constexpr int kLW = kLightDeg;               // light list capacity
 constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 // per light warp: R[kLW], La[kLW], Ba[kLB], Bb[kLB], Bl[kLB]
-constexpr int kAPcap = 1024;                 // heavy: positions of R adjacent to a, kept for the fast loops
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
 constexpr int kPool = 896;                   // light: staged list entries, R's lists then L_a's lists
 constexpr int kFW = 32;                      // light: 1024-bit membership filters of R and of L_a
@@ -133,12 +131,6 @@ __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x)
 __device__ __forceinline__ uint32_t swap2(uint32_t c) { return ((c & 1u) << 1) | (c >> 1); }
 __device__ __forceinline__ uint32_t get2(const uint32_t *B, int p) { return (B[p >> 4] >> ((p & 15) << 1)) & 3u; }
 __device__ __forceinline__ void set2(uint32_t *B, int p, uint32_t code) { atomicOr(B + (p >> 4), code << ((p & 15) << 1)); }
-
-template <int NW>
-__device__ __forceinline__ void team_sync() {
-    if constexpr (NW == 1) __syncwarp();
-    else __syncthreads();
-}
 
 // predicated fire-and-forget u64 add (no divergent branch around it in the uniform b loops)
 __device__ __forceinline__ void red_if(bool p, unsigned long long *addr, uint32_t v) {
@@ -281,20 +273,18 @@ __device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, 
 
 // Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
 // al = a's list.  Run by one warp.  Returns |L_a|.
-__device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
-                       int lane, uint32_t *AP = nullptr, int *nap = nullptr, const uint32_t *FR = nullptr) {
-    // AP (optional): the positions of R adjacent to a, ascending (*nap = their number)
-    int nL = 0, nA = 0;
+__device__ int build_a(uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La, int lane,
+                       const uint32_t *FR) {
+    int nL = 0;
     for (int base = 0; base < al.len; base += 32) {
         const int p = base + lane;
         bool keep = false;
-        int pos = -1;
         uint32_t e = 0;
         if (p < al.len) {
             e = al.p[p];
             const uint32_t x = e >> 2;
             if (x > r) {
-                pos = fmay(FR, x) ? find_rank(R, D, x) : -1;
+                const int pos = fmay(FR, x) ? find_rank(R, D, x) : -1;
                 if (pos >= 0) set2(Ba, pos, e & 3u);
                 else keep = true;
             }
@@ -302,87 +292,56 @@ __device__ int build_a(const Dev &g, uint32_t r, List al, const uint32_t *R, int
         const unsigned bal = __ballot_sync(kFull, keep);
         if (keep) La[nL + __popc(bal & ((1u << lane) - 1u))] = e;
         nL += __popc(bal);
-        if (AP) {
-            const unsigned bp = __ballot_sync(kFull, pos >= 0);
-            const int slot = nA + __popc(bp & ((1u << lane) - 1u));
-            if (pos >= 0 && slot < kAPcap) AP[slot] = (uint32_t)pos;   // caller ignores AP if nA > kAPcap
-            nA += __popc(bp);
-        }
     }
     __syncwarp();
-    if (nap) *nap = nA;
     return nL;
 }
 
 // Phase A of a heavy task, by the whole CTA: a's list in 32-entry groups, warp w takes groups
-// w, w + NW, ...  Pass 1 scatters code(a, x), x in R, into Ba and records per group the ballots
-// of its L_a entries and of its entries in R; warp 0 scans the group counts; pass 2 writes La
-// (sorted: list order) and AP (positions of R adjacent to a, ascending, first kAPcap).
-// tmp: 4 * ceil(len / 32) words of zeroed scratch, NOT re-zeroed here (the caller clears it).
-// *s_nL = |L_a|, *s_nap = |AP| (may exceed kAPcap).  Ends with a barrier.
+// w, w + NW, ...  Pass 1 scatters code(a, x), x in R, into Ba and records per group the ballot
+// of its L_a entries; warp 0 scans the group counts; pass 2 writes La (sorted: list order).
+// tmp: 2 * ceil(len / 32) words of scratch.  *s_nL = |L_a|.  Ends with a barrier.
 template <int NW>
-__device__ void build_a_cta(const Dev &g, uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La,
-                            uint32_t *AP, uint32_t *tmp, int *s_nL, int *s_nap, int wid, int lane) {
+__device__ void build_a_cta(uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La, uint32_t *tmp,
+                            int *s_nL, int wid, int lane) {
     const int G = (al.len + 31) >> 5;
-    uint32_t *KM = tmp, *AM = tmp + G, *KO = tmp + 2 * G, *AO = tmp + 3 * G;
+    uint32_t *KM = tmp, *KO = tmp + G;
     for (int gi = wid; gi < G; gi += NW) {
         const int p = gi * 32 + lane;
-        bool keep = false, inR = false;
+        bool keep = false;
         if (p < al.len) {
             const uint32_t e = al.p[p], x = e >> 2;
             if (x > r) {
                 const int pos = find_rank(R, D, x);
-                if (pos >= 0) {
-                    set2(Ba, pos, e & 3u);
-                    inR = true;
-                } else {
-                    keep = true;
-                }
+                if (pos >= 0) set2(Ba, pos, e & 3u);
+                else keep = true;
             }
         }
-        const unsigned km = __ballot_sync(kFull, keep), am = __ballot_sync(kFull, inR);
-        if (lane == 0) {
-            KM[gi] = km;
-            AM[gi] = am;
-        }
+        const unsigned km = __ballot_sync(kFull, keep);
+        if (lane == 0) KM[gi] = km;
     }
     __syncthreads();
     if (wid == 0) {
-        int bk = 0, ba = 0;
+        int bk = 0;
         for (int g0 = 0; g0 < G; g0 += 32) {
             const int gi = g0 + lane;
-            const int ck = gi < G ? __popc(KM[gi]) : 0, ca = gi < G ? __popc(AM[gi]) : 0;
-            int ik = ck, ia = ca;
+            const int ck = gi < G ? __popc(KM[gi]) : 0;
+            int ik = ck;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const int yk = __shfl_up_sync(kFull, ik, d), ya = __shfl_up_sync(kFull, ia, d);
-                if (lane >= d) {
-                    ik += yk;
-                    ia += ya;
-                }
+                const int yk = __shfl_up_sync(kFull, ik, d);
+                if (lane >= d) ik += yk;
             }
-            if (gi < G) {
-                KO[gi] = (uint32_t)(bk + ik - ck);
-                AO[gi] = (uint32_t)(ba + ia - ca);
-            }
+            if (gi < G) KO[gi] = (uint32_t)(bk + ik - ck);
             bk += __shfl_sync(kFull, ik, 31);
-            ba += __shfl_sync(kFull, ia, 31);
         }
-        if (lane == 0) {
-            *s_nL = bk;
-            *s_nap = ba;
-        }
+        if (lane == 0) *s_nL = bk;
     }
     __syncthreads();
     const unsigned lt = (1u << lane) - 1u;
     for (int gi = wid; gi < G; gi += NW) {
-        const unsigned km = KM[gi], am = AM[gi];
-        const int p = gi * 32 + lane;
-        if (km >> lane & 1u) La[KO[gi] + __popc(km & lt)] = al.p[p];
-        if (am >> lane & 1u) {
-            const uint32_t slot = AO[gi] + __popc(am & lt);
-            if (slot < (uint32_t)kAPcap) AP[slot] = (uint32_t)find_rank(R, D, al.p[p] >> 2);
-        }
+        const unsigned km = KM[gi];
+        if (km >> lane & 1u) La[KO[gi] + __popc(km & lt)] = al.p[gi * 32 + lane];
     }
     __syncthreads();
 }
@@ -793,7 +752,7 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
 // U, corrected per c at its events; R[j] gets, from key lanes 0..2, the number of the chunk's
 // c's with that key; an x-R[j] edge makes every set of that j non-plain (classified alone), an
 // R[j]-c edge makes c's PART 1 set non-plain and removes its PART 2 set (c is in N(a)).
-constexpr int kCrossBlock = 512;    // default j-block length g.xblock (<= kMaxBlock: the 10-bit count fields)
+constexpr int kCrossBlock = 256;    // default j-block length g.xblock (<= kMaxBlock: the 10-bit count fields)
 
 // c's R-neighbour list pointer: next entry (position of R, code(c, R[pos])) with position < jend
 __device__ __forceinline__ void ca_next(const uint32_t *CA, uint32_t q1, uint32_t &q, uint32_t &npos) {
@@ -1007,8 +966,7 @@ template <int K, int C, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
-                                           int *s_ca, const Staged *st, const uint32_t *AP, int nap, int w,
-                                           int lane) {
+                                           int *s_ca, const Staged *st, int w, int lane) {
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -1097,7 +1055,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item;
-    __shared__ int s_nL, s_work, s_ca[2], s_nap;   // s_ca: CA space used, next c of ca_build
+    __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
@@ -1109,7 +1067,6 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         uint32_t *hb = HSMEM ? sm : g.gheavy + (int64_t)blockIdx.x * g.gheavy_per_cta;
         uint32_t *R = hb + L.R, *La = hb + L.La, *Ba = hb + L.Ba;
         uint32_t *Bl = hb + L.Bl + wid * L.lw;
-        uint32_t *AP = hb + L.AP;   // positions of R adjacent to a (kAPcap)
         uint8_t *codes = reinterpret_cast<uint8_t *>(hb + L.Bb);   // heavy: per-task code bytes
         if (!HSMEM) {   // zero this CTA's global bitmaps once
             for (int q = tid; q < L.Bl + kWarps * L.lw - L.Ba; q += kBlock) hb[L.Ba + q] = 0;
@@ -1134,9 +1091,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
             }
             const List al = glist(g, R[i] >> 2);
-            build_a_cta<kWarps>(g, r, al, R, D, Ba, La, AP, hb + L.Bl, &s_nL, &s_nap, wid, lane);
+            build_a_cta<kWarps>(r, al, R, D, Ba, La, hb + L.Bl, &s_nL, wid, lane);
             const int nL = s_nL;
-            for (int q = tid; q < 4 * ((al.len + 31) >> 5); q += kBlock) hb[L.Bl + q] = 0;   // build_a_cta scratch
+            for (int q = tid; q < 2 * ((al.len + 31) >> 5); q += kBlock) hb[L.Bl + q] = 0;   // build_a_cta scratch
             if (tid == 0) {
                 s_work = 0;
                 s_ca[0] = 0;
@@ -1146,8 +1103,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, AP,
-                                  s_nap <= kAPcap ? s_nap : -1, wid, lane);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
@@ -1201,14 +1157,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     clear_words(Bl, 0, (al.len + 15) >> 4, lane);
                     __syncwarp();
                 }
-                const int nL = build_a(g, r, al, R, D, Ba, La, lane, nullptr, nullptr, FR);
+                const int nL = build_a(r, al, R, D, Ba, La, lane, FR);
                 FL[lane] = 0;
                 __syncwarp();
                 for (int q = lane; q < nL; q += 32) fadd(FL, La[q] >> 2);
                 __syncwarp();
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
                 task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
-                                 nullptr, -1, 0, lane);
+                                    0, lane);
                 flush_hist<C>(H, g, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
@@ -1351,8 +1307,7 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
     L.Ba = L.La + md;
     L.Bb = L.Ba + L.bw;                  // heavy: the per-task code bytes (md bytes)
     L.Bl = L.Bb + (md + 3) / 4;
-    L.AP = L.Bl + kWarps * L.lw;
-    const int heavy_words = L.AP + kAPcap;
+    const int heavy_words = L.Bl + kWarps * L.lw;
     const int light_words = kWarps * kLightWords;
     const int hist_words = kWarps * C;
     const int budget_words = (104 * 1024) / 4 - hist_words;   // keep 2 CTAs per SM
