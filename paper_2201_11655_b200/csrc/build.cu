@@ -3,7 +3,8 @@
 //
 // S1 ("G_U ... ignoring the direction"; P:81 simple graphs; P:125-134 CSR):
 //   every arc u -> v yields two G_U entries, (u, v, code 1) and (v, u, code 2), packed in a
-//   64-bit key  owner << 34 | nbr << 2 | code.  One radix sort groups each unordered pair's
+//   64-bit key  owner << (vb + 2) | nbr << 2 | code  (vb = bits of a vertex id; the sorts read
+//   only bits [2, 2 vb + 2): 6 radix passes at n = 5M).  One radix sort groups each unordered pair's
 //   entries; OR-merging equal (owner, nbr) keys gives ONE entry per G_U edge with both
 //   direction bits (a mutual pair is a single entry with code 3 -- reading G14).
 // S2: rank = undirected degree descending, ties by ascending id (G2/G3).
@@ -30,7 +31,7 @@ inline unsigned grid_for(int64_t work) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64));
 }
 
-__global__ void k_arc_keys(int64_t m, int64_t n, const int32_t *__restrict__ src,
+__global__ void k_arc_keys(int64_t m, int64_t n, int vb, const int32_t *__restrict__ src,
                            const int32_t *__restrict__ dst, uint64_t *__restrict__ keys,
                            unsigned long long *__restrict__ bad) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
@@ -42,8 +43,8 @@ __global__ void k_arc_keys(int64_t m, int64_t n, const int32_t *__restrict__ src
             u = 0;
             v = 1;
         }
-        keys[2 * e] = ((uint64_t)u << 34) | ((uint64_t)v << 2) | 1u;       // owner u, u -> v
-        keys[2 * e + 1] = ((uint64_t)v << 34) | ((uint64_t)u << 2) | 2u;   // owner v, u -> v = nbr -> owner
+        keys[2 * e] = ((uint64_t)u << (vb + 2)) | ((uint64_t)v << 2) | 1u;       // owner u, u -> v
+        keys[2 * e + 1] = ((uint64_t)v << (vb + 2)) | ((uint64_t)u << 2) | 2u;   // owner v, nbr -> owner
     }
 }
 
@@ -54,7 +55,7 @@ __global__ void k_heads(int64_t len, const uint64_t *__restrict__ keys, int32_t 
 }
 
 // merged[pos[i]] = pair key | OR of the run's codes; deg[owner]++
-__global__ void k_merge(int64_t len, const uint64_t *__restrict__ keys, const int32_t *__restrict__ head,
+__global__ void k_merge(int64_t len, int vb, const uint64_t *__restrict__ keys, const int32_t *__restrict__ head,
                         const int64_t *__restrict__ pos, uint64_t *__restrict__ merged, int32_t *__restrict__ deg,
                         unsigned long long *__restrict__ arcs) {
     unsigned long long local_arcs = 0;
@@ -64,7 +65,7 @@ __global__ void k_merge(int64_t len, const uint64_t *__restrict__ keys, const in
         uint64_t code = k & 3;
         for (int64_t j = i + 1; j < len && (keys[j] >> 2) == (k >> 2); j++) code |= keys[j] & 3;
         merged[pos[i]] = (k & ~3ull) | code;
-        atomicAdd(&deg[k >> 34], 1);
+        atomicAdd(&deg[k >> (vb + 2)], 1);
         local_arcs += code & 1;   // count each arc once, from its tail's entry
     }
     atomicAdd(arcs, local_arcs);
@@ -89,19 +90,21 @@ __global__ void k_order_from_rank(int64_t n, const int32_t *__restrict__ rank, i
         order[rank[v]] = (int32_t)v;
 }
 
-__global__ void k_relabel(int64_t nnz, const uint64_t *__restrict__ merged, const int32_t *__restrict__ rank,
+__global__ void k_relabel(int64_t nnz, int vb, const uint64_t *__restrict__ merged, const int32_t *__restrict__ rank,
                           uint64_t *__restrict__ keys, int32_t *__restrict__ deg_r) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t k = merged[i];
-        uint64_t ro = (uint64_t)rank[k >> 34], rn = (uint64_t)rank[(k >> 2) & 0xffffffffull];
-        keys[i] = (ro << 34) | (rn << 2) | (k & 3);
+        const uint64_t vmask = (1ull << vb) - 1ull;
+        uint64_t ro = (uint64_t)rank[k >> (vb + 2)], rn = (uint64_t)rank[(k >> 2) & vmask];
+        keys[i] = (ro << (vb + 2)) | (rn << 2) | (k & 3);
         atomicAdd(&deg_r[ro], 1);
     }
 }
 
-__global__ void k_adj(int64_t nnz, const uint64_t *__restrict__ keys, uint32_t *__restrict__ adj) {
+__global__ void k_adj(int64_t nnz, int vb, const uint64_t *__restrict__ keys, uint32_t *__restrict__ adj) {
+    const uint64_t mask = (1ull << (vb + 2)) - 1ull;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
-        adj[i] = (uint32_t)(keys[i] & 0xffffffffull);   // rank(nbr) << 2 | code  (rank < 2^30)
+        adj[i] = (uint32_t)(keys[i] & mask);   // rank(nbr) << 2 | code  (rank < 2^30)
 }
 
 // split[v] = first entry of v's list with rank > v;  fwd[v] = forward degree
@@ -179,16 +182,16 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
 
     // ---- S1: entries, sort, OR-merge
     if (m > 0) {
-        k_arc_keys<<<grid_for(m), kThreads, 0, s>>>(m, n, d_src, d_dst, keys, flags);
+        k_arc_keys<<<grid_for(m), kThreads, 0, s>>>(m, n, vb, d_src, d_dst, keys, flags);
         VDMC_LAUNCH();
         size_t tb = 0;
         void *tstore = nullptr;
         cub::DoubleBuffer<uint64_t> db(keys, keys2);
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)L, 0, 34 + vb, s));
+        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)L, 2, 2 * vb + 2, s));
         VDMC_CUDA(tmp.alloc((char **)&tstore, tb));
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(tstore, tb, db, (int)L, 0, 34 + vb, s));
+        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(tstore, tb, db, (int)L, 2, 2 * vb + 2, s));
         trace("sort1 enqueued");
-        count_launch(2 * ((34 + vb + 7) / 8));
+        count_launch(2 * ((2 * vb + 7) / 8));
         uint64_t *sorted = db.Current();
         k_heads<<<grid_for(L), kThreads, 0, s>>>(L, sorted, head);
         VDMC_LAUNCH();
@@ -201,7 +204,7 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
         // nnz = pos[L-1] + head[L-1]
         uint64_t *mbuf = (sorted == keys) ? keys2 : keys;   // free half of the double buffer
         merged = mbuf;
-        k_merge<<<grid_for(L), kThreads, 0, s>>>(L, sorted, head, pos, merged, deg, flags + 1);
+        k_merge<<<grid_for(L), kThreads, 0, s>>>(L, vb, sorted, head, pos, merged, deg, flags + 1);
         VDMC_LAUNCH();
         int64_t last_pos = 0;
         int32_t last_head = 0;
@@ -256,16 +259,16 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     VDMC_CUDA(cudaMemsetAsync(g->tfirst, 0, sizeof(int64_t) * (n + 1), s));
     if (nnz > 0) {
         uint64_t *rl = (merged == keys) ? keys2 : keys;
-        k_relabel<<<grid_for(nnz), kThreads, 0, s>>>(nnz, merged, rank, rl, deg_r);
+        k_relabel<<<grid_for(nnz), kThreads, 0, s>>>(nnz, vb, merged, rank, rl, deg_r);
         VDMC_LAUNCH();
         cub::DoubleBuffer<uint64_t> db(rl, merged);
         size_t tb = 0;
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)nnz, 0, 34 + vb, s));
+        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)nnz, 2, 2 * vb + 2, s));
         void *ts = nullptr;
         VDMC_CUDA(tmp.alloc((char **)&ts, tb));
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(ts, tb, db, (int)nnz, 0, 34 + vb, s));
-        count_launch(2 * ((34 + vb + 7) / 8));
-        k_adj<<<grid_for(nnz), kThreads, 0, s>>>(nnz, db.Current(), g->adj);
+        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(ts, tb, db, (int)nnz, 2, 2 * vb + 2, s));
+        count_launch(2 * ((2 * vb + 7) / 8));
+        k_adj<<<grid_for(nnz), kThreads, 0, s>>>(nnz, vb, db.Current(), g->adj);
         trace("sort2 enqueued");
         VDMC_LAUNCH();
     }
