@@ -36,3 +36,23 @@ def test_reference_arm_torchrun_world2():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_line_gpu_small():
+    """bench.py's own arm on the GPU (small config): one JSON line with the contract's keys."""
+    r = subprocess.run([sys.executable, "bench.py", "--config", "cfg3", "--k", "3", "--steps", "2", "--warmup", "3",
+                        "--e2e-steps", "1", "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    (line,) = _lines(r.stdout)
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["steps"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["roofline"]["bound"] in ("alu", "hbm") and 0 < line["roofline"]["frac"] < 1
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert "workload" in line["config"]
