@@ -70,6 +70,8 @@ struct Dev {
     int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
     int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields)
     int xblock;                               // cross items: positions per item (<= kMaxBlock)
+    int minrem;                               // profiling only: skip heavy tasks with D - i - 1 < minrem
+                                              // (minrem < 0: skip those with D - i - 1 >= -minrem)
     uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
     int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
     uint32_t ca_cap;
@@ -1085,6 +1087,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int64_t rs = g.split[r];
             const int D = (int)(g.off[r + 1] - rs);
             const int i = (int)(t - g.tfirst[r]);
+            if (g.minrem > 0 ? D - i - 1 < g.minrem : (g.minrem < 0 && D - i - 1 >= -g.minrem)) continue;   // VDMC_MINREM
             if (staged != r) {
                 for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
                 staged = r;
@@ -1529,6 +1532,9 @@ static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int6
     }
     if (const char *sk = getenv("VDMC_SKIP")) {   // profiling only; results incomplete
         d.skip = atoi(sk);
+    }
+    if (const char *mr = getenv("VDMC_MINREM")) {   // profiling only; results incomplete
+        d.minrem = atoi(mr);
     }
     d.fold = kMaxBlock;
     d.xblock = kCrossBlock;

@@ -25,11 +25,17 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("xblock 256", {"VDMC_XBLOCK": "256"}),
             ("xblock 1023", {"VDMC_XBLOCK": "1023"}),
             ("star block 512", {"VDMC_FOLD": "512"}), ("star block 256", {"VDMC_FOLD": "256"}),
-            ("star 512 xblock 256", {"VDMC_FOLD": "512", "VDMC_XBLOCK": "256"})]
+            ("star 512 xblock 256", {"VDMC_FOLD": "512", "VDMC_XBLOCK": "256"}),
+            ("heavy, only tasks with >= 128 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "128"}),
+            ("heavy, only tasks with < 128 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "-128"}),
+            ("heavy, only tasks with >= 512 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "512"}),
+            ("heavy, only tasks with < 512 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "-512"})]
 if len(sys.argv) > 3 and sys.argv[3] == "quick":
     variants = variants[:3]
+elif len(sys.argv) > 3 and sys.argv[3] == "tasks":
+    variants = variants[:2] + [v for v in variants if "VDMC_MINREM" in v[1]]
 for label, env in variants:
-    for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_XBLOCK", "VDMC_FOLD"):
+    for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_XBLOCK", "VDMC_FOLD", "VDMC_MINREM"):
         os.environ.pop(key, None)
     os.environ.update(env)
     ts = []
