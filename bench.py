@@ -33,13 +33,12 @@ sys.path.insert(0, ROOT)
 import graphgen as G  # noqa: E402
 
 METRIC = "4-motif per-vertex counting: motifs/sec and edges/sec at 1/2/4/8 B200"
-BYTES_PER_MOTIF = {3: 36, 4: 52}   # 4 B neighbour entry + (k-1) x 16 B u64 RMW
+# per motif, the neighbour entry yielding its last member (4 B) plus one u64
+# read-modify-write (16 B) per counter atomic that reaches L2.  B_k,eff = 4 + 16 x (L2 atomic /
+# reduction requests per motif), the requests measured by ncu on the same workload
+# (profiles/ncu_traffic.json, lts__t_requests_op_{red,atom}.sum); B_k = 4 + 16 (k-1) when no
+# member is aggregated.
 FALLBACK_HBM = 6650.0             # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
-# Which resource bounds k_enum, by graph family (ncu, profiles/r01_*): on the power-law graphs the
-# hub-leaf counter rows stay in L2 (DRAM at ~13% of peak) and the kernel is integer-issue bound;
-# on Erdos-Renyi the per-set counter updates scatter over a matrix >> L2 and HBM sectors bound it.
-BOUND = {"ba": "alu", "gnp": "hbm"}
-LANES_PER_SM = 128                # 4 SMSPs x 32 lanes: one integer op per lane per clock (issue limit)
 
 
 def parse():
@@ -55,6 +54,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--virtual-parts", type=int, default=0,
+                   help="planner balance on one GPU: time each of G cost-balanced slices (vdmc_plan) back "
+                        "to back and print max/mean (not the contract line)")
     return p.parse_args()
 
 
@@ -67,23 +69,14 @@ def peak_hbm():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-def peak_alu(nsm):
-    """Integer issue peak, int-op/s: SMs x 128 lanes x max SM clock (MEASURED_PEAKS.json sm_max_mhz)."""
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            mhz, src = float(json.load(f)["sm_max_mhz"]), "MEASURED_PEAKS.json sm_max_mhz"
-    except Exception:
-        mhz, src = 1965.0, "B200 max SM clock 1965 MHz (fallback)"
-    return nsm * LANES_PER_SM * mhz * 1e6, f"{nsm} SMs x {LANES_PER_SM} int lanes x {mhz:.0f} MHz ({src})"
-
-
-def ncu_traffic(config, k):
-    """Per-launch DRAM bytes of the enumeration kernel from the committed ncu summary."""
+def ncu_counters(config, k, kind):
+    """Per-launch ncu counters of the enumeration kernel on this workload (committed summary,
+    profiles/ncu_traffic.json, written by tools/ncu_counters.py from one --set full capture)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"{config}-k{k}", {}).get("dram_bytes_per_launch")
+        return d.get(f"{config}-k{k}" + ("-undirected" if kind == "undirected" else ""))
     except Exception:
         return None
 
@@ -140,6 +133,17 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def cpu_cores():
@@ -199,11 +203,45 @@ def run_reference(args, world, rank):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS[args.config]['desc']}", "k": k, "n": n,
                    "arcs": int(g[1].size), "parallelism": "host cores (oracle, OpenMP)"},
-        "cpu_baseline": {"value": value, "unit": "motifs/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": "motifs/s", "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"ESU over roots with random label < {hi} of {n} ({tot // args.steps} sets/step)"},
         "e2e": {"value": value, "unit": "motifs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_virtual_parts(args):
+    """SURVEY §8(e) on one GPU: the G slices of vdmc_plan counted one after another; the
+    slowest slice bounds a G-GPU step, so max/mean is the planner's balance."""
+    import torch
+    from paper_2201_11655_b200 import vdmc
+    k = args.k or G.CONFIGS[args.config]["k"][-1]
+    n, src, dst = G.make_config(args.config)
+    g = vdmc.Graph(n, torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda())
+    G_ = args.virtual_parts
+    parts = g.plan(k, G_)
+    full = g.count(k, kind=args.kind)
+    tm = {}
+    g.count(k, kind=args.kind, timings=tm)
+    acc = torch.zeros_like(full)
+    per = []
+    for rep in range(max(1, args.steps)):
+        ms = []
+        for sl in parts:
+            t = {}
+            out = g.count(k, work=sl, kind=args.kind, timings=t)
+            if rep == 0:
+                acc += out
+            ms.append(t["enum"])
+            del out
+        per.append(ms)
+    assert torch.equal(acc, full), "slice partials do not sum to the full matrix"
+    ms = [min(x) for x in zip(*per)]
+    line = {"mode": "virtual-parts", "config": args.config, "k": k, "kind": args.kind, "parts": G_,
+            "slices": parts, "slice_enum_ms": ms, "max_over_mean": max(ms) / (sum(ms) / len(ms)),
+            "full_enum_ms": tm["enum"], "ideal_speedup": tm["enum"] / max(ms), "sum_equals_full": True}
+    print(json.dumps(line), flush=True)
+    g.close()
 
 
 def main():
@@ -212,6 +250,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
+    if args.virtual_parts:
+        run_virtual_parts(args)
+        return
     import torch
     import torch.distributed as dist
     from paper_2201_11655_b200 import vdmc
@@ -219,9 +260,12 @@ def main():
     k = args.k or G.CONFIGS[args.config]["k"][-1]
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        comm = vdmc.Comm(device=local)   # libvdmc's own NCCL communicator (vdmc_count_distributed)
     stream = torch.cuda.current_stream()
+    args.warmup = max(1, args.warmup)
 
     n, src, dst = G.make_config(args.config)
     arcs = int(src.size)
@@ -229,27 +273,25 @@ def main():
     d_dst = torch.from_numpy(dst).to(dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)   # 256 MiB > 126 MB L2
 
-    def step(e_src, e_dst, out_host=None):
+    def step(e_src, e_dst, out_host=None, tm=None):
         g = vdmc.Graph(n, e_src, e_dst, device=local)
-        g.set_profiling(True)
-        work = g.plan(k, world)[rank] if world > 1 else None
-        out = g.count(k, work=work, kind=args.kind)
         if world > 1:
-            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM)
-        if out_host is not None and rank == 0:
+            out = vdmc.count_distributed(g, k, comm, root=0, kind=args.kind)
+        else:
+            out = g.count(k, kind=args.kind, timings=tm)
+        if out_host is not None and out is not None:
             out_host.copy_(out, non_blocking=True)
         return g, out
 
-    # warm-up (also yields the result the metric is computed from)
+    def motifs_of(out):
+        colsum = out.sum(dim=0).cpu().numpy().view(np.uint64).astype(object)
+        return int(sum(colsum)) // k
+
     for _ in range(args.warmup):
         g, out = step(d_src, d_dst)
         g.close()
+        del out
     torch.cuda.synchronize()
-    total_sets = None
-    if rank == 0:
-        colsum = out.sum(dim=0).cpu().numpy().view(np.uint64).astype(object)
-        total_sets = int(sum(colsum)) // k
-    del out
 
     # ---- timed region: K steps, device events per step, L2 flushed between steps
     if world > 1:
@@ -257,19 +299,23 @@ def main():
     torch.cuda.synchronize()
     clocks = Clocks(local) if rank == 0 else None
     launches0 = vdmc.kernel_launches()
-    step_ms, enum_ms, phase_ms = [], [], []
+    step_ms, enum_ms, phase_ms, motifs = [], [], [], []
     for _ in range(args.steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        tm = {} if world == 1 else None
         e0.record(stream)
-        g, out = step(d_src, d_dst)
+        g, out = step(d_src, d_dst, tm=tm)
         e1.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        tm = g.timings()
-        enum_ms.append(tm["enum"])
-        phase_ms.append(tm)
+        build_ms = g.info["build_ms"]
+        if tm:
+            enum_ms.append(tm["enum"])
+            phase_ms.append({"build": build_ms, **tm})
+        if out is not None:
+            motifs.append(motifs_of(out))   # from this step's own result (outside the timed events)
         g.close()
         del out
     launches = vdmc.kernel_launches() - launches0
@@ -314,60 +360,84 @@ def main():
     if world > 1:
         dist.all_reduce(E, op=dist.ReduceOp.MAX)
     E_ms = float(E.item()) / max(1, args.e2e_steps)
+    if rank == 0:
+        e2e_motifs = motifs_of(h_out)
+        assert e2e_motifs == motifs[0], "e2e result differs from the device-resident steps"
 
     if rank == 0:
+        assert len(set(motifs)) == 1, f"motif totals differ between steps: {motifs}"
+        total_sets = motifs[0]
         ms_per_step = T_ms / args.steps
         value = total_sets / (ms_per_step / 1e3)
         peak, peak_src = peak_hbm()
-        enum_avg = statistics.mean(enum_ms)
-        # roofline of the dominant kernel (the enumeration), per launch; this rank's share of the
-        # motifs approximated by 1/world.  hbm: algorithmic bytes = motifs x B_k.
-        # alu: algorithmic integer ops = motifs x k, the k member increments of P:118.
-        traffic = ncu_traffic(args.config, k)
-        motifs_launch = total_sets / world
-        bound = BOUND[G.CONFIGS[args.config]["kind"]]
-        if bound == "hbm":
-            achieved = motifs_launch * BYTES_PER_MOTIF[k] / (enum_avg / 1e3) / 1e9
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": traffic, "peak_source": peak_src,
-                    "algorithmic": f"{BYTES_PER_MOTIF[k]} B per motif (SURVEY 8(d) M3) x {motifs_launch:.4g} motifs"}
-        else:
-            palu, palu_src = peak_alu(torch.cuda.get_device_properties(dev).multi_processor_count)
-            achieved = motifs_launch * k / (enum_avg / 1e3) / 1e12
-            roof = {"bound": "alu", "achieved": achieved, "peak": palu / 1e12, "unit": "Tint-op/s",
-                    "frac": achieved * 1e12 / palu, "traffic": traffic, "peak_source": palu_src,
-                    "algorithmic": f"{k} counter increments per motif (P:118) x {motifs_launch:.4g} motifs",
-                    "hbm_achieved_model_GBs": motifs_launch * BYTES_PER_MOTIF[k] / (enum_avg / 1e3) / 1e9}
-        roof["kernel"] = f"k_enum<{k}>"
-        if traffic:
-            roof["traffic_GBs"] = traffic / (enum_avg / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": "motifs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "edges_per_sec": arcs / (ms_per_step / 1e3),
             "motifs_per_step": total_sets,
+            "step_ms": {"mean": ms_per_step, "median": statistics.median(step_ms), "best": min(step_ms),
+                        "all": step_ms},
             "config": {"workload": f"{args.config}: {G.CONFIGS[args.config]['desc']}", "k": k, "n": n,
-                       "arcs": arcs, "motif_kind": args.kind, "parallelism": f"dp{world} (graph replicated, task slices, NCCL reduce)"
+                       "arcs": arcs, "motif_kind": args.kind,
+                       "parallelism": f"dp{world} (graph replicated, cost-balanced task slices, ncclReduce)"
                        if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write); count matrix >> L2"},
-            "kernel_ms": {"enum_avg": enum_avg, "step_avg": ms_per_step, "enum_share": enum_avg / ms_per_step,
-                          **{f"{key}_avg": statistics.mean(t[key] for t in phase_ms)
-                             for key in ("build", "plan", "finalize")}},
-            "roofline": roof,
             "e2e": {"value": total_sets / (E_ms / 1e3), "unit": "motifs/s",
                     "h2d_bytes_per_step": int(2 * 4 * arcs),
                     "d2h_bytes_per_step": int(n * C * 8), "ms_per_step": E_ms},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        if enum_ms:
+            enum_avg = statistics.mean(enum_ms)
+            line["kernel_ms"] = {"enum_avg": enum_avg, "enum_median": statistics.median(enum_ms),
+                                 "enum_best": min(enum_ms), "step_avg": ms_per_step,
+                                 "enum_share": enum_avg / ms_per_step,
+                                 **{f"{key}_avg": statistics.mean(t[key] for t in phase_ms)
+                                    for key in ("build", "schedule", "finalize")}}
+            line["roofline"] = roofline(args, k, total_sets, enum_avg, peak, peak_src)
         if world == 1 and not args.no_cpu_baseline:
             rate, sets, dt, hi, cores = oracle_sample((n, src, dst), k, args.cpu_seconds)
             line["cpu_baseline"] = {"value": rate, "unit": "motifs/s", "cores": cores, "kind": "oracle",
+                                    "cpu": cpu_model(),
                                     "sample": f"ESU, roots with random label < {hi} of {n}: {sets} sets in {dt:.1f} s"}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline(args, k, motifs, enum_ms, peak, peak_src):
+    """SURVEY §8(d) roofline of the dominant kernel (k_enum), per launch (N = 1).
+    frac     : M3 model, algorithmic bytes = motifs x B_k,eff over the live kernel time, vs the
+               measured HBM copy bandwidth.  B_k,eff = 4 + 16 x (L2 atomic/reduction requests per
+               motif) from ncu on this workload.
+    dram_frac: measured DRAM bytes per launch (ncu) over the live kernel time, vs the same peak.
+    issue_frac: warp instructions issued / (SMSPs x cycles) in the ncu capture."""
+    t = enum_ms / 1e3
+    c = ncu_counters(args.config, k, args.kind)
+    roof = {"bound": "hbm", "kernel": f"k_enum<{k}>", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+            "motifs_per_launch": motifs}
+    b_full = 4 + 16 * (k - 1)
+    roof["B_k"] = b_full
+    roof["frac_B_k"] = motifs * b_full / t / 1e9 / peak
+    if c:
+        atoms = c["l2_red_requests"] + c["l2_atom_requests"]
+        b_eff = 4 + 16 * atoms / motifs
+        achieved = motifs * b_eff / t / 1e9
+        roof.update({"achieved": achieved, "frac": achieved / peak, "B_k_eff": b_eff,
+                     "atomics_per_motif": atoms / motifs, "traffic": c["dram_bytes"],
+                     "dram_GBs": c["dram_bytes"] / t / 1e9, "dram_frac": c["dram_bytes"] / t / 1e9 / peak,
+                     "issue_frac": c.get("issue_frac"), "l2_hit_pct": c.get("l2_hit_pct"),
+                     "l2_red_hit_pct": c.get("l2_red_hit_pct"), "warps_active_pct": c.get("warps_active_pct"),
+                     "ncu_source": c.get("report"),
+                     "algorithmic": f"motifs x B_k,eff = {motifs:.4g} x {b_eff:.2f} B (SURVEY 8(d) M3)"})
+    else:
+        roof.update({"achieved": None, "frac": None, "traffic": None,
+                     "note": "no ncu counters committed for this workload (profiles/ncu_traffic.json)"})
+    return roof
 
 
 if __name__ == "__main__":

@@ -3,8 +3,8 @@
 The computation lives in ``lib/libvdmc.so`` (CUDA sm_100a, C ABI in ``include/vdmc.h``);
 ``vdmc`` is the thin ctypes binding.  See DESIGN.md.
 """
-from .vdmc import (Graph, VdmcError, class_ids, count, count_distributed, kernel_launches,  # noqa: F401
-                   num_classes, split_costs)
+from .vdmc import (Comm, Graph, VdmcError, class_ids, count, count_distributed,  # noqa: F401
+                   count_slices_reduce, kernel_launches, num_classes, split_costs, symmetrize)
 
-__all__ = ["Graph", "VdmcError", "class_ids", "count", "count_distributed", "kernel_launches",
-           "num_classes", "split_costs"]
+__all__ = ["Comm", "Graph", "VdmcError", "class_ids", "count", "count_distributed", "count_slices_reduce",
+           "kernel_launches", "num_classes", "split_costs", "symmetrize"]

@@ -10,6 +10,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nccl.h>
+
 #include "vdmc_internal.cuh"
 
 namespace vdmc {
@@ -365,6 +367,72 @@ vdmc_status vdmc_build_graph(int64_t n, const int64_t *indptr, const int32_t *nb
     return vdmc_build_graph_edges(n, (int64_t)s.size(), s.data(), d.data(), 0, rank, device, nullptr, out);
 }
 
+vdmc_status vdmc_symmetrize(int64_t n, const int64_t *out_indptr, const int32_t *out_nbr, int device,
+                            int64_t **indptr, int32_t **nbr, uint8_t **dir) {
+    if (!out_indptr || !indptr || !nbr || !dir) return fail(VDMC_EINVAL, "NULL argument");
+    if (n < 0 || n >= (int64_t(1) << 30)) return fail(VDMC_EINVAL, "n=%lld outside [0, 2^30)", (long long)n);
+    if (out_indptr[0] != 0) return fail(VDMC_EINVAL, "Indices[0] != 0");
+    for (int64_t v = 0; v < n; v++)
+        if (out_indptr[v + 1] < out_indptr[v]) return fail(VDMC_EINVAL, "Indices decreases at vertex %lld", (long long)v);
+    const int64_t m = out_indptr[n];
+    if (m > 0 && !out_nbr) return fail(VDMC_EINVAL, "Neighbors is NULL");
+    // the paper's CSR row v lists the heads of v's arcs: expand to the arc list
+    std::vector<int32_t> src((size_t)m), dst((size_t)m);
+    for (int64_t v = 0; v < n; v++)
+        for (int64_t e = out_indptr[v]; e < out_indptr[v + 1]; e++) {
+            const int32_t u = out_nbr[e];
+            if (u < 0 || u >= n)
+                return fail(VDMC_ERANGE, "vertex %lld: out-neighbour %d outside [0,%lld)", (long long)v, u, (long long)n);
+            if (u == v) return fail(VDMC_ESELFLOOP, "self-loop at vertex %lld", (long long)v);
+            src[(size_t)e] = (int32_t)v;
+            dst[(size_t)e] = u;
+        }
+    vdmc_status st = check_device(device);
+    if (st) return st;
+    VDMC_CUDA(cudaSetDevice(device));
+    cudaStream_t s = nullptr;
+    int32_t *d = nullptr;
+    VDMC_CUDA(dalloc((void **)&d, sizeof(int32_t) * 2 * std::max<int64_t>(m, 1), s));
+    if (m) {
+        VDMC_CUDA(cudaMemcpyAsync(d, src.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+        VDMC_CUDA(cudaMemcpyAsync(d + m, dst.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+    }
+    int64_t nnz = 0;
+    uint64_t *ent = nullptr;
+    int vb = 0;
+    st = symmetrize_device(n, m, d, d + m, s, &nnz, &ent, &vb);
+    dfree(d, s);
+    if (st) return st;
+    std::vector<uint64_t> h((size_t)nnz);
+    cudaError_t ce = nnz ? cudaMemcpy(h.data(), ent, sizeof(uint64_t) * nnz, cudaMemcpyDeviceToHost) : cudaSuccess;
+    dfree(ent, s);
+    VDMC_CUDA(ce);
+    int64_t *ip = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    int32_t *nb = (int32_t *)malloc(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+    uint8_t *dc = (uint8_t *)malloc(std::max<int64_t>(nnz, 1));
+    if (!ip || !nb || !dc) {
+        free(ip);
+        free(nb);
+        free(dc);
+        return fail(VDMC_ENOMEM, "host allocation of %lld entries failed", (long long)nnz);
+    }
+    // entries: owner << (vb + 2) | nbr << 2 | code, sorted by (owner, nbr)
+    const uint64_t vmask = (1ull << vb) - 1ull;
+    for (int64_t v = 0; v <= n; v++) ip[v] = 0;
+    for (int64_t e = 0; e < nnz; e++) {
+        ip[(h[e] >> (vb + 2)) + 1]++;
+        nb[e] = (int32_t)((h[e] >> 2) & vmask);
+        dc[e] = (uint8_t)(h[e] & 3u);
+    }
+    for (int64_t v = 0; v < n; v++) ip[v + 1] += ip[v];
+    *indptr = ip;
+    *nbr = nb;
+    *dir = dc;
+    return VDMC_OK;
+}
+
+void vdmc_free_host(void *p) { free(p); }
+
 vdmc_status vdmc_get_info(const vdmc_graph *g, vdmc_graph_info *info) {
     if (!g || !info) return fail(VDMC_EINVAL, "NULL argument");
     info->n = g->n;
@@ -373,6 +441,7 @@ vdmc_status vdmc_get_info(const vdmc_graph *g, vdmc_graph_info *info) {
     info->ntasks = g->ntasks;
     info->max_degree = g->max_degree;
     info->device = g->device;
+    info->build_ms = g->build_ms;
     return VDMC_OK;
 }
 
@@ -383,12 +452,30 @@ vdmc_status vdmc_get_order(const vdmc_graph *g, int32_t *order) {
     return VDMC_OK;
 }
 
-vdmc_status vdmc_count_kind(vdmc_graph *g, int k, int kind, uint64_t *counts, const vdmc_range *work, void *stream) {
+static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o) {
     if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
-    if (kind != VDMC_DIRECTED && kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", kind);
-    if (!g) return fail(VDMC_EINVAL, "graph is NULL");
-    if (!counts && g->n > 0) return fail(VDMC_EINVAL, "counts is NULL");
-    int64_t lo = 0, hi = g->ntasks;
+    if (!opt) return VDMC_OK;
+    if (opt->kind != VDMC_DIRECTED && opt->kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", opt->kind);
+    if (opt->star_block < 0 || opt->star_block > 1023) return fail(VDMC_EINVAL, "star_block=%d not in [1,1023] (0 = default)", opt->star_block);
+    if (opt->cross_block != 0 && (opt->cross_block < 32 || opt->cross_block > 1023))
+        return fail(VDMC_EINVAL, "cross_block=%d not in [32,1023] (0 = default)", opt->cross_block);
+    if (opt->heavy_global < 0 || opt->heavy_global > 1 || opt->force_big < 0 || opt->force_big > 1)
+        return fail(VDMC_EINVAL, "heavy_global / force_big must be 0 or 1");
+    if (opt->ca_capacity < 0 || opt->ca_capacity > (int64_t(1) << 30))
+        return fail(VDMC_EINVAL, "ca_capacity=%lld not in [1, 2^30] (0 = default)", (long long)opt->ca_capacity);
+    o.kind = opt->kind;
+    o.star_block = opt->star_block;
+    o.cross_block = opt->cross_block;
+    o.heavy_global = opt->heavy_global;
+    o.force_big = opt->force_big;
+    o.ca_capacity = opt->ca_capacity;
+    o.timings_ms = opt->timings_ms;
+    return VDMC_OK;
+}
+
+static vdmc_status check_work(const vdmc_graph *g, const vdmc_range *work, int64_t &lo, int64_t &hi) {
+    lo = 0;
+    hi = g->ntasks;
     if (work) {
         if (work->task_lo < 0 || work->task_hi < work->task_lo || work->task_hi > g->ntasks)
             return fail(VDMC_EINVAL, "work slice [%lld,%lld) not inside [0,%lld)", (long long)work->task_lo,
@@ -396,12 +483,77 @@ vdmc_status vdmc_count_kind(vdmc_graph *g, int k, int kind, uint64_t *counts, co
         lo = work->task_lo;
         hi = work->task_hi;
     }
-    VDMC_CUDA(cudaSetDevice(g->device));
-    return launch_count(g, k, kind, counts, lo, hi, (cudaStream_t)stream);
+    return VDMC_OK;
 }
 
-vdmc_status vdmc_count(vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work, void *stream) {
-    return vdmc_count_kind(g, k, VDMC_DIRECTED, counts, work, stream);
+// one count: per-call class-major accumulator (block cache), enumerate, finalise
+static vdmc_status count_impl(const vdmc_graph *g, int k, const CountOpts &o, uint64_t *counts, int64_t lo, int64_t hi,
+                              cudaStream_t s) {
+    const int C = num_classes(k, o.kind);
+    float ms3[2] = {0, 0};
+    cudaEvent_t ev[3] = {};
+    if (o.timings_ms) {
+        for (auto &e : ev) VDMC_CUDA(cudaEventCreate(&e));
+        VDMC_CUDA(cudaEventRecord(ev[0], s));
+    }
+    unsigned long long *acc = nullptr;
+    VDMC_CUDA(dalloc((void **)&acc, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
+    vdmc_status st = count_into(g, k, o, acc, lo, hi, s, o.timings_ms ? ms3 : nullptr);
+    if (st == VDMC_OK) {
+        if (o.timings_ms) cudaEventRecord(ev[1], s);
+        st = finalize(g, C, acc, counts, s);
+        if (o.timings_ms) cudaEventRecord(ev[2], s);
+    }
+    dfree(acc, s);
+    if (o.timings_ms) {
+        if (st == VDMC_OK) {
+            cudaEventSynchronize(ev[2]);
+            float fin = 0, all = 0;
+            cudaEventElapsedTime(&fin, ev[1], ev[2]);
+            cudaEventElapsedTime(&all, ev[0], ev[2]);
+            o.timings_ms[0] = ms3[0];
+            o.timings_ms[1] = ms3[1];
+            o.timings_ms[2] = fin;
+            o.timings_ms[3] = all;
+        }
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+    return st;
+}
+
+vdmc_status vdmc_count_ex(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
+                          const vdmc_count_options *opt, void *stream) {
+    CountOpts o;
+    vdmc_status st = check_opts(k, opt, o);
+    if (st) return st;
+    if (!g) return fail(VDMC_EINVAL, "graph is NULL");
+    if (!counts && g->n > 0) return fail(VDMC_EINVAL, "counts is NULL");
+    int64_t lo, hi;
+    if ((st = check_work(g, work, lo, hi))) return st;
+    VDMC_CUDA(cudaSetDevice(g->device));
+    return count_impl(g, k, o, counts, lo, hi, (cudaStream_t)stream);
+}
+
+vdmc_status vdmc_count_kind(const vdmc_graph *g, int k, int kind, uint64_t *counts, const vdmc_range *work,
+                            void *stream) {
+    vdmc_count_options o{};
+    o.kind = kind;
+    return vdmc_count_ex(g, k, counts, work, &o, stream);
+}
+
+vdmc_status vdmc_count(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work, void *stream) {
+    return vdmc_count_ex(g, k, counts, work, nullptr, stream);
+}
+
+vdmc_status vdmc_root_range(const vdmc_graph *g, int64_t pos_lo, int64_t pos_hi, vdmc_range *out) {
+    if (!g || !out) return fail(VDMC_EINVAL, "NULL argument");
+    if (pos_lo < 0 || pos_hi < pos_lo || pos_hi > g->n)
+        return fail(VDMC_EINVAL, "positions [%lld,%lld) not inside [0,%lld]", (long long)pos_lo, (long long)pos_hi,
+                    (long long)g->n);
+    VDMC_CUDA(cudaSetDevice(g->device));
+    VDMC_CUDA(cudaMemcpy(&out->task_lo, g->tfirst + pos_lo, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    VDMC_CUDA(cudaMemcpy(&out->task_hi, g->tfirst + pos_hi, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return VDMC_OK;
 }
 
 vdmc_status vdmc_split_costs(const int64_t *prefix, int64_t ntasks, int nparts, vdmc_range *parts) {
@@ -425,44 +577,90 @@ vdmc_status vdmc_split_costs(const int64_t *prefix, int64_t ntasks, int nparts, 
     return VDMC_OK;
 }
 
-vdmc_status vdmc_plan(vdmc_graph *g, int k, int nparts, vdmc_range *parts) {
+vdmc_status vdmc_plan(const vdmc_graph *g, int k, int nparts, vdmc_range *parts) {
     if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
     if (!g || nparts < 1 || !parts) return fail(VDMC_EINVAL, "bad arguments to vdmc_plan");
     VDMC_CUDA(cudaSetDevice(g->device));
-    vdmc_status st = ensure_plan(g, k, nullptr);
-    if (st) return st;
     std::vector<int64_t> prefix((size_t)g->ntasks);
-    if (g->ntasks) VDMC_CUDA(cudaMemcpy(prefix.data(), g->cost, sizeof(int64_t) * g->ntasks, cudaMemcpyDeviceToHost));
+    vdmc_status st = plan_prefix(g, k, prefix.data(), nullptr);
+    if (st) return st;
     return vdmc_split_costs(prefix.data(), g->ntasks, nparts, parts);
 }
 
-vdmc_status vdmc_set_profiling(vdmc_graph *g, int on) {
-    if (!g) return fail(VDMC_EINVAL, "graph is NULL");
-    VDMC_CUDA(cudaSetDevice(g->device));
-    if (on && !g->ev[0])
-        for (auto &e : g->ev) VDMC_CUDA(cudaEventCreate(&e));
-    g->profiling = on ? 1 : 0;
+// ------------------------------------------------------------------ multi-GPU (NCCL)
+struct vdmc_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0, device = 0;
+};
+
+#define VDMC_NCCL(call)                                                                              \
+    do {                                                                                             \
+        ncclResult_t r_ = (call);                                                                    \
+        if (r_ != ncclSuccess) return fail(VDMC_ENCCL, "%s: %s", #call, ncclGetErrorString(r_));       \
+    } while (0)
+
+vdmc_status vdmc_comm_unique_id(uint8_t id[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    if (!id) return fail(VDMC_EINVAL, "id is NULL");
+    ncclUniqueId u;
+    VDMC_NCCL(ncclGetUniqueId(&u));
+    memcpy(id, &u, sizeof u);
     return VDMC_OK;
 }
 
-vdmc_status vdmc_last_timings(const vdmc_graph *g, float *ms, int nms) {
-    if (!g || !ms || nms < 0 || nms > 5) return fail(VDMC_EINVAL, "bad arguments to vdmc_last_timings");
-    vdmc_graph *gg = const_cast<vdmc_graph *>(g);
-    if (g->profiling && g->ev[0]) {
-        VDMC_CUDA(cudaSetDevice(g->device));
-        // events: 0 count start, 1 plan done, 2 enum done, 3 finalize done
-        float t[3];
-        VDMC_CUDA(cudaEventElapsedTime(&t[0], g->ev[0], g->ev[1]));
-        VDMC_CUDA(cudaEventElapsedTime(&t[1], g->ev[1], g->ev[2]));
-        VDMC_CUDA(cudaEventElapsedTime(&t[2], g->ev[2], g->ev[3]));
-        gg->last_ms[1] = t[0];
-        gg->last_ms[2] = t[1];
-        gg->last_ms[3] = t[2];
-        gg->last_ms[4] = t[0] + t[1] + t[2];
-    }
-    gg->last_ms[0] = g->build_ms;
-    for (int i = 0; i < nms; i++) ms[i] = g->last_ms[i];
+vdmc_status vdmc_comm_init(int nranks, int rank, const uint8_t id[128], int device, vdmc_comm **out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(VDMC_EINVAL, "bad arguments to vdmc_comm_init");
+    vdmc_status st = check_device(device);
+    if (st) return st;
+    VDMC_CUDA(cudaSetDevice(device));
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof u);
+    ncclComm_t c = nullptr;
+    VDMC_NCCL(ncclCommInitRank(&c, nranks, u, rank));
+    vdmc_comm *h = new vdmc_comm();
+    h->comm = c;
+    h->nranks = nranks;
+    h->rank = rank;
+    h->device = device;
+    *out = h;
     return VDMC_OK;
+}
+
+void vdmc_comm_free(vdmc_comm *c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+vdmc_status vdmc_count_distributed(const vdmc_graph *g, int k, const vdmc_count_options *opt, vdmc_comm *comm,
+                                   int root, uint64_t *counts, void *stream) {
+    CountOpts o;
+    vdmc_status st = check_opts(k, opt, o);
+    if (st) return st;
+    if (!g || !comm) return fail(VDMC_EINVAL, "NULL graph or communicator");
+    if (root < 0 || root >= comm->nranks) return fail(VDMC_EINVAL, "root %d not in [0,%d)", root, comm->nranks);
+    if (comm->device != g->device) return fail(VDMC_EINVAL, "graph on device %d, communicator on %d", g->device, comm->device);
+    if (comm->rank == root && !counts && g->n > 0) return fail(VDMC_EINVAL, "counts is NULL on the root rank");
+    VDMC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<vdmc_range> parts((size_t)comm->nranks);
+    if ((st = vdmc_plan(g, k, comm->nranks, parts.data()))) return st;
+    const vdmc_range my = parts[(size_t)comm->rank];
+    const int C = num_classes(k, o.kind);
+    const size_t elems = (size_t)std::max<int64_t>(g->n, 1) * C;
+    unsigned long long *acc = nullptr;
+    VDMC_CUDA(dalloc((void **)&acc, elems * sizeof(uint64_t), s));
+    o.timings_ms = nullptr;
+    st = count_into(g, k, o, acc, my.task_lo, my.task_hi, s, nullptr);
+    if (st == VDMC_OK) {
+        // sum of the class-major partials (uint64 wrap-around addition: exact), then the root
+        // restores rows in place of original ids
+        ncclResult_t r = ncclReduce(acc, acc, elems, ncclUint64, ncclSum, root, comm->comm, s);
+        if (r != ncclSuccess) st = fail(VDMC_ENCCL, "ncclReduce: %s", ncclGetErrorString(r));
+        else if (comm->rank == root) st = finalize(g, C, acc, counts, s);
+    }
+    dfree(acc, s);
+    return st;
 }
 
 vdmc_status vdmc_trim(int device) {
@@ -478,13 +676,11 @@ void vdmc_free_graph(vdmc_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
-    void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->acc,
-                    g->lscratch, g->ctr, g->lut[0][0], g->lut[0][1], g->lut[1][0], g->lut[1][1], g->cost, g->heavy_task, g->light_root,
-                    g->hroots, g->hbase, g->nr_off, g->nr_adj};
+    void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->lut[0][0], g->lut[0][1],
+                    g->lut[1][0], g->lut[1][1], g->heavy_task, g->light_root, g->hroots, g->hbase, g->nr_off,
+                    g->nr_adj};
     for (void *p : ptrs) dfree(p, nullptr);
     cudaStreamSynchronize(nullptr);
-    for (auto &e : g->ev)
-        if (e) cudaEventDestroy(e);
     delete g;
 }
 

@@ -150,6 +150,90 @@ int bits_for(int64_t x) {   // bits needed to hold values in [0, x)
 
 }  // namespace
 
+// S1 on the device: arcs -> one G_U entry per (owner, nbr) pair with the OR of its direction
+// codes, sorted by (owner, nbr) in ORIGINAL ids.  merged (length nnz) is one half of the
+// caller's double buffer keys/keys2 [2m]; deg[owner] counts entries (G_U degree).
+static vdmc_status s1_entries(int64_t n, int64_t m, int vb, const int32_t *d_src, const int32_t *d_dst,
+                              cudaStream_t s, Tmp &tmp, uint64_t *keys, uint64_t *keys2, int32_t *deg,
+                              uint64_t **merged_out, int64_t *nnz_out, int64_t *arcs_out) {
+    const int64_t L = 2 * m;
+    *merged_out = nullptr;
+    *nnz_out = 0;
+    *arcs_out = 0;
+    if (m <= 0) return VDMC_OK;
+    int32_t *head = nullptr;
+    int64_t *pos = nullptr;
+    unsigned long long *flags = nullptr;   // [0] first bad arc, [1] arc count
+    VDMC_CUDA(tmp.alloc(&head, L));
+    VDMC_CUDA(tmp.alloc(&pos, L));
+    VDMC_CUDA(tmp.alloc(&flags, 2));
+    VDMC_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
+    VDMC_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(unsigned long long), s));
+    k_arc_keys<<<grid_for(m), kThreads, 0, s>>>(m, n, vb, d_src, d_dst, keys, flags);
+    VDMC_LAUNCH();
+    size_t tb = 0;
+    void *tstore = nullptr;
+    cub::DoubleBuffer<uint64_t> db(keys, keys2);
+    VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)L, 2, 2 * vb + 2, s));
+    VDMC_CUDA(tmp.alloc((char **)&tstore, tb));
+    VDMC_CUDA(cub::DeviceRadixSort::SortKeys(tstore, tb, db, (int)L, 2, 2 * vb + 2, s));
+    trace("sort1 enqueued");
+    count_launch(2 * ((2 * vb + 7) / 8));
+    uint64_t *sorted = db.Current();
+    k_heads<<<grid_for(L), kThreads, 0, s>>>(L, sorted, head);
+    VDMC_LAUNCH();
+    size_t tb2 = 0;
+    VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, head, pos, (int)L, s));
+    void *tstore2 = nullptr;
+    VDMC_CUDA(tmp.alloc((char **)&tstore2, tb2));
+    VDMC_CUDA(cub::DeviceScan::ExclusiveSum(tstore2, tb2, head, pos, (int)L, s));
+    count_launch(2);
+    uint64_t *merged = (sorted == keys) ? keys2 : keys;   // free half of the double buffer
+    k_merge<<<grid_for(L), kThreads, 0, s>>>(L, vb, sorted, head, pos, merged, deg, flags + 1);
+    VDMC_LAUNCH();
+    int64_t last_pos = 0;
+    int32_t last_head = 0;
+    unsigned long long hf[2];
+    VDMC_CUDA(cudaMemcpyAsync(&last_pos, pos + L - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    VDMC_CUDA(cudaMemcpyAsync(&last_head, head + L - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    VDMC_CUDA(cudaMemcpyAsync(hf, flags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    VDMC_CUDA(cudaStreamSynchronize(s));
+    trace("sync after merge");
+    if (hf[0] != ~0ull) {
+        long long e = (long long)(hf[0] >> 2);
+        if ((hf[0] & 3) == 1) return fail(VDMC_ESELFLOOP, "arc %lld is a self-loop", e);
+        return fail(VDMC_ERANGE, "arc %lld has a vertex id outside [0, %lld)", e, (long long)n);
+    }
+    *merged_out = merged;
+    *nnz_out = last_pos + last_head;
+    *arcs_out = (int64_t)hf[1];
+    return VDMC_OK;
+}
+
+vdmc_status symmetrize_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, cudaStream_t s,
+                              int64_t *nnz_out, uint64_t **d_entries, int *vb_out) {
+    Tmp tmp(s);
+    const int vb = bits_for(std::max<int64_t>(n, 2));
+    uint64_t *keys = nullptr, *keys2 = nullptr;
+    int32_t *deg = nullptr;
+    VDMC_CUDA(tmp.alloc(&keys, 2 * m));
+    VDMC_CUDA(tmp.alloc(&keys2, 2 * m));
+    VDMC_CUDA(tmp.alloc(&deg, n));
+    VDMC_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    uint64_t *merged = nullptr;
+    int64_t nnz = 0, arcs = 0;
+    vdmc_status st = s1_entries(n, m, vb, d_src, d_dst, s, tmp, keys, keys2, deg, &merged, &nnz, &arcs);
+    if (st) return st;
+    uint64_t *out = nullptr;
+    VDMC_CUDA(dalloc((void **)&out, sizeof(uint64_t) * std::max<int64_t>(nnz, 1), s));
+    if (nnz) VDMC_CUDA(cudaMemcpyAsync(out, merged, sizeof(uint64_t) * nnz, cudaMemcpyDeviceToDevice, s));
+    VDMC_CUDA(cudaStreamSynchronize(s));
+    *nnz_out = nnz;
+    *d_entries = out;
+    *vb_out = vb;
+    return VDMC_OK;
+}
+
 vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, const int32_t *h_rank,
                          int device, cudaStream_t s, vdmc_graph *g) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -162,65 +246,22 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     const int vb = bits_for(std::max<int64_t>(n, 2));
     const int64_t L = 2 * m;
     uint64_t *keys = nullptr, *keys2 = nullptr, *merged = nullptr;
-    int32_t *head = nullptr, *deg = nullptr, *rank = nullptr, *deg_r = nullptr;
-    int64_t *pos = nullptr, *fwd = nullptr;
-    unsigned long long *flags = nullptr;   // [0] first bad arc, [1] arc count, [2] nnz
+    int32_t *deg = nullptr, *rank = nullptr, *deg_r = nullptr;
+    int64_t *fwd = nullptr;
     VDMC_CUDA(tmp.alloc(&keys, L));
     VDMC_CUDA(tmp.alloc(&keys2, L));
-    VDMC_CUDA(tmp.alloc(&head, L));
-    VDMC_CUDA(tmp.alloc(&pos, L));
     VDMC_CUDA(tmp.alloc(&deg, n));
     VDMC_CUDA(tmp.alloc(&deg_r, n));
     VDMC_CUDA(tmp.alloc(&rank, n));
     VDMC_CUDA(tmp.alloc(&fwd, n));
-    VDMC_CUDA(tmp.alloc(&flags, 4));
-    VDMC_CUDA(cudaMemsetAsync(flags, 0xff, sizeof(unsigned long long), s));
-    VDMC_CUDA(cudaMemsetAsync(flags + 1, 0, 3 * sizeof(unsigned long long), s));
     VDMC_CUDA(cudaMemsetAsync(deg, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
     VDMC_CUDA(cudaMemsetAsync(deg_r, 0, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
     trace("build allocs+memsets");
 
     // ---- S1: entries, sort, OR-merge
-    if (m > 0) {
-        k_arc_keys<<<grid_for(m), kThreads, 0, s>>>(m, n, vb, d_src, d_dst, keys, flags);
-        VDMC_LAUNCH();
-        size_t tb = 0;
-        void *tstore = nullptr;
-        cub::DoubleBuffer<uint64_t> db(keys, keys2);
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int)L, 2, 2 * vb + 2, s));
-        VDMC_CUDA(tmp.alloc((char **)&tstore, tb));
-        VDMC_CUDA(cub::DeviceRadixSort::SortKeys(tstore, tb, db, (int)L, 2, 2 * vb + 2, s));
-        trace("sort1 enqueued");
-        count_launch(2 * ((2 * vb + 7) / 8));
-        uint64_t *sorted = db.Current();
-        k_heads<<<grid_for(L), kThreads, 0, s>>>(L, sorted, head);
-        VDMC_LAUNCH();
-        size_t tb2 = 0;
-        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, head, pos, (int)L, s));
-        void *tstore2 = nullptr;
-        VDMC_CUDA(tmp.alloc((char **)&tstore2, tb2));
-        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(tstore2, tb2, head, pos, (int)L, s));
-        count_launch(2);
-        // nnz = pos[L-1] + head[L-1]
-        uint64_t *mbuf = (sorted == keys) ? keys2 : keys;   // free half of the double buffer
-        merged = mbuf;
-        k_merge<<<grid_for(L), kThreads, 0, s>>>(L, vb, sorted, head, pos, merged, deg, flags + 1);
-        VDMC_LAUNCH();
-        int64_t last_pos = 0;
-        int32_t last_head = 0;
-        unsigned long long hf[2];
-        VDMC_CUDA(cudaMemcpyAsync(&last_pos, pos + L - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        VDMC_CUDA(cudaMemcpyAsync(&last_head, head + L - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        VDMC_CUDA(cudaMemcpyAsync(hf, flags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-        VDMC_CUDA(cudaStreamSynchronize(s));
-        trace("sync after merge");
-        if (hf[0] != ~0ull) {
-            long long e = (long long)(hf[0] >> 2);
-            if ((hf[0] & 3) == 1) return fail(VDMC_ESELFLOOP, "arc %lld is a self-loop", e);
-            return fail(VDMC_ERANGE, "arc %lld has a vertex id outside [0, %lld)", e, (long long)n);
-        }
-        g->nnz = last_pos + last_head;
-        g->arcs = (int64_t)hf[1];
+    {
+        vdmc_status st = s1_entries(n, m, vb, d_src, d_dst, s, tmp, keys, keys2, deg, &merged, &g->nnz, &g->arcs);
+        if (st) return st;
     }
     const int64_t nnz = g->nnz;
 
@@ -307,6 +348,10 @@ vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32
     if (g->ntasks > 0) {
         k_task_root<<<grid_for(n * 32), kThreads, 0, s>>>(n, g->tfirst, g->task_root);
         VDMC_LAUNCH();
+    }
+    {   // S3 device LUTs + S4 schedule (heavy/light lists, induced adjacency of heavy roots)
+        vdmc_status st = build_schedule(g, s);
+        if (st) return st;
     }
     VDMC_CUDA(cudaEventRecord(e1, s));
     VDMC_CUDA(cudaStreamSynchronize(s));

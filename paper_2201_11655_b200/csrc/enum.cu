@@ -49,6 +49,14 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
 
+// Profiling switches that DROP work (VDMC_PHASES / VDMC_SKIP / VDMC_MINREM) exist only in the
+// profiling build (-DVDMC_PROFILING, tools/build_variant.sh); the product library has none.
+#ifdef VDMC_PROFILING
+#define VDMC_SKIPF(g) ((g).skip)
+#else
+#define VDMC_SKIPF(g) 0
+#endif
+
 struct Dev {
     const int64_t *__restrict__ off;
     const int64_t *__restrict__ split;
@@ -64,14 +72,16 @@ struct Dev {
     uint32_t *__restrict__ glight;            // global fallback: per-warp oversize L_a + bitmap
     int64_t gheavy_per_cta, glight_per_warp;  // words
     int heavy_in_smem;                        // heavy buffers fit in shared memory
-    int big;                                  // degrees so large a task could overflow u32 histograms
+    int big;                                  // flush the u32 histograms per item (degrees > 32767, or forced)
     int maxdeg;
     int off32;                                // n * C < 2^32: 32-bit accumulator offsets
-    int skip;                                 // profiling only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
     int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields)
     int xblock;                               // cross items: positions per item (<= kMaxBlock)
-    int minrem;                               // profiling only: skip heavy tasks with D - i - 1 < minrem
+#ifdef VDMC_PROFILING
+    int skip;                                 // profiling build only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
+    int minrem;                               // profiling build only: skip heavy tasks with D - i - 1 < minrem
                                               // (minrem < 0: skip those with D - i - 1 >= -minrem)
+#endif
     uint32_t *__restrict__ gca;               // per-CTA: c's R-neighbour lists of a heavy task (cross items)
     int64_t gca_per_cta;                      // words: CAbeg[maxdeg], CAlen[maxdeg], CA[ca_cap]
     uint32_t ca_cap;
@@ -904,9 +914,55 @@ __device__ __forceinline__ void cross_item(const Dev &g, const uint8_t *lut, uin
     __syncwarp();
 }
 
+// The "2+1" sets of the task (r, x = R[i]) for one c = L_x[q], used when the task's c
+// R-neighbour lists do not fit the CA scratch.  It keeps the cross items' partition (a set
+// {r, a < b, c} belongs to the task of the depth-1 vertex c hangs off first: a if c ~ a, else
+// b), so tasks of one root may mix both paths: one lane per position j of R,
+//   PART 1, j > i:  {r, a = x, b = R[j], c}           (every j)
+//   PART 2, j < i:  {r, a = R[j], b = x, c}           (only if c is not adjacent to R[j])
+// code(c, R[j]) is scattered from c's list into the warp's 2-bit bitmap Bw first.
+template <int C>
+__device__ __forceinline__ void cross_c_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
+                                             int D, const uint8_t *codes, const uint32_t *La, int q, uint32_t *Bw,
+                                             uint32_t *H, uint32_t cra, uint32_t x, int lane) {
+    const uint32_t ec = La[q], c = ec >> 2, cxc = ec & 3u;
+    const int64_t c0 = g.off[c], c1 = g.off[c + 1];
+    bool any = false;
+    for (int64_t base = c0; base < c1; base += 32) {
+        const int64_t p = base + lane;
+        if (p < c1) {
+            const uint32_t e = g.adj[p];
+            if ((e >> 2) > r) {
+                const int pos = find_rank(R, D, e >> 2);
+                if (pos >= 0 && pos != i) {
+                    set2(Bw, pos, e & 3u);
+                    any = true;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    for (int base = 0; base < D; base += 32) {
+        const int j = base + lane;
+        int col = kNone;
+        uint32_t b = 0;
+        if (j < D && j != i) {
+            const uint32_t e = R[j], crj = e & 3u, cxj = (uint32_t)codes[j] >> 2, ccj = get2(Bw, j);
+            b = e >> 2;
+            if (j > i) col = lut[cra | crj << 2 | cxj << 6 | cxc << 8 | swap2(ccj) << 10];
+            else if (ccj == 0u) col = lut[crj | cra << 2 | swap2(cxj) << 6 | cxc << 10];
+        }
+        emit4<C>(H, g, c, b, col, lane);   // c warp-uniform, R[j] per lane
+    }
+    __syncwarp();
+    if (__any_sync(kFull, any)) clear_words(Bw, 0, (D + 15) >> 4, lane);
+    if (g.big) flush_hist<C>(H, g, r, x, lane);
+    __syncwarp();
+}
+
 // c's R-neighbour lists (positions ascending, x = R[i] excluded, code(c, R[pos])) for every c
 // in L_x, into the CTA scratch; each warp walks the lists of its c's twice (count, write).
-// Returns false if they do not fit (the task then falls back to item_b_in_R).
+// Returns false if they do not fit (the task then runs cross_c_item per c instead).
 template <int NW>
 __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const uint32_t *R, int D,
                                          const uint32_t *La, int nL, uint32_t *CAbeg, uint32_t *CAlen, uint32_t *CA,
@@ -997,20 +1053,20 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         }
         if (g.big) flush_hist<C>(H, g, r, a, lane);
     } else if constexpr (NW == 1) {
-        for (int j = i + 1; !(g.skip & 2) && j < D; j++)
+        for (int j = i + 1; !(VDMC_SKIPF(g) & 2) && j < D; j++)
             item_b_in_R<C, 1>(g, lut, r, i, j, R, D, Ba, La, nL, Bb, Bl, H, cra, a,
                               list_at(g, R, j, st->RL, st->RS, st->rok), lane, st->FR, st->FL);
-        for (int x = 0; !(g.skip & 4) && x < nL; x++)
+        for (int x = 0; !(VDMC_SKIPF(g) & 4) && x < nL; x++)
             item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, list_at(g, La, x, st->LL, st->LS, st->lok),
                             lane, st->FR, st->FL);
     } else {
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
-        const bool cross = !(g.skip & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
+        const bool cross = !(VDMC_SKIPF(g) & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
         int nstar = 0;   // star items: chunk x block of b positions
         for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, g.fold);
         const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
-        const int nB = cross ? nck * njb : D - 1 - i;                           // "2+1" items
+        const int nB = cross ? nck * njb : nL;                                  // "2+1" items
         const int total = nstar + nB + nL;
         // star items (bounded length), then the "2+1" items, then the b-in-L_a items
         for (;;) {
@@ -1032,17 +1088,16 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                 b_it = it - nstar;
             }
             if (star_k >= 0) {
-                if (!(g.skip & 1)) star_item<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, star_b, lane);
+                if (!(VDMC_SKIPF(g) & 1)) star_item<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, star_b, lane);
             } else if (b_it >= 0) {
-                if (g.skip & 2) continue;
+                if (VDMC_SKIPF(g) & 2) continue;
                 if (cross)
                     cross_item<C>(g, lut, r, i, R, D, codes, La, nL, CAbeg, CAlen, CA, cra, a, H, b_it / njb,
                                   b_it % njb, lane);
                 else
-                    item_b_in_R<C, NW>(g, lut, r, i, i + 1 + b_it, R, D, Ba, La, nL, nullptr, Bl, H, cra, a,
-                                       glist(g, R[i + 1 + b_it] >> 2), lane);
+                    cross_c_item<C>(g, lut, r, i, R, D, codes, La, b_it, Bl, H, cra, a, lane);
             } else {
-                if (!(g.skip & 4))
+                if (!(VDMC_SKIPF(g) & 4))
                     item_b_in_La<C>(g, lut, r, it - nstar - nB, R, D, La, nL, Bl, H, cra, a,
                                     glist(g, La[it - nstar - nB] >> 2), lane);
             }
@@ -1056,12 +1111,29 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     constexpr int NM = K == 3 ? 64 : 4096;
     extern __shared__ uint32_t sm[];
     __shared__ uint8_t lut[NM];
-    __shared__ int64_t s_item;
+    __shared__ int64_t s_item, s_sub[4];   // s_sub: the slice's heavy_task [h0, h1) and light_root [l0, l1)
     __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
     uint32_t *H = sm + L.hist + wid * C;
+    if (tid < 4) {   // both lists ascend with the task id, so the slice [lo, hi) is a sub-list of each
+        const bool heavy = tid < 2;
+        const int64_t key = (tid & 1) ? hi : lo;
+        int64_t a = 0, b = heavy ? g.nheavy : g.nlight;
+        while (a < b) {   // first entry whose tasks end after key (heavy: task >= key; light: tfirst[r+1] > key
+            const int64_t mid = (a + b) >> 1;   // for lo, tfirst[r] >= key for hi)
+            bool before;
+            if (heavy) before = g.heavy_task[mid] < key;
+            else {
+                const int64_t r = g.light_root[mid];
+                before = (tid & 1) ? g.tfirst[r] < key : g.tfirst[r + 1] <= key;
+            }
+            if (before) a = mid + 1;
+            else b = mid;
+        }
+        s_sub[tid] = a;
+    }
 
     // ---------------- heavy phase: one CTA per task (r, a)
     {
@@ -1075,19 +1147,20 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         }
         __syncthreads();
         int64_t staged = -1;
-        for (;;) {
-            if (tid == 0) s_item = (int64_t)atomicAdd(ctr, 1ull);
+        for (;;) {   // bounds re-read from shared memory (keeps them out of the loop's registers)
+            if (tid == 0) s_item = s_sub[0] + (int64_t)atomicAdd(ctr, 1ull);
             __syncthreads();
             const int64_t h = s_item;
             __syncthreads();
-            if (h >= g.nheavy) break;
+            if (h >= s_sub[1]) break;
             const int64_t t = g.heavy_task[h];
-            if (t < lo || t >= hi) continue;
             const uint32_t r = (uint32_t)g.task_root[t];
             const int64_t rs = g.split[r];
             const int D = (int)(g.off[r + 1] - rs);
             const int i = (int)(t - g.tfirst[r]);
+#ifdef VDMC_PROFILING
             if (g.minrem > 0 ? D - i - 1 < g.minrem : (g.minrem < 0 && D - i - 1 >= -g.minrem)) continue;   // VDMC_MINREM
+#endif
             if (staged != r) {
                 for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
                 staged = r;
@@ -1129,8 +1202,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         for (;;) {
             unsigned long long x = 0;
             if (lane == 0) x = atomicAdd(ctr + 1, 1ull);
-            const int64_t li = (int64_t)__shfl_sync(kFull, x, 0);
-            if (li >= g.nlight) break;
+            const int64_t li = s_sub[2] + (int64_t)__shfl_sync(kFull, x, 0);
+            if (li >= s_sub[3]) break;
             const uint32_t r = (uint32_t)g.light_root[li];
             const int64_t t0 = g.tfirst[r], t1 = g.tfirst[r + 1];
             const int64_t ta = max(t0, lo), tb = min(t1, hi);
@@ -1325,72 +1398,53 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
 
 }  // namespace
 
-vdmc_status ensure_acc(vdmc_graph *g, int k, int kind, cudaStream_t s) {
-    const int C = num_classes(k, kind);
-    const size_t need = (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t);
-    if (g->acc_bytes < need) {
-        dfree(g->acc, s);
-        g->acc = nullptr;
-        g->acc_bytes = 0;
-        VDMC_CUDA(dalloc((void **)&g->acc, need, s));
-        g->acc_bytes = need;
-    }
-    if (!g->ctr) VDMC_CUDA(dalloc((void **)&g->ctr, 4 * sizeof(unsigned long long), s));
-    uint8_t *&lut = g->lut[kind][k == 4 ? 1 : 0];
-    if (!lut) {
-        const size_t nm = k == 3 ? 64 : 4096;
-        VDMC_CUDA(dalloc((void **)&lut, nm, s));
-        VDMC_CUDA(cudaMemcpyAsync(lut, host_lut(k, kind), nm, cudaMemcpyHostToDevice, s));
-    }
-    return VDMC_OK;
-}
-
-// heavy / light work lists (S4 schedule), cached in the graph
-static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
-    if (g->roots_ready) return VDMC_OK;
+// S3 (device copies of the class LUTs) + S4 schedule, built once per graph at the end of a build:
+// heavy / light work lists and the induced adjacency of every heavy root's N+(r).
+vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s) {
+    for (int kind = 0; kind < 2; kind++)
+        for (int k4 = 0; k4 < 2; k4++) {
+            const size_t nm = k4 ? 4096 : 64;
+            VDMC_CUDA(dalloc((void **)&g->lut[kind][k4], nm, s));
+            VDMC_CUDA(cudaMemcpyAsync(g->lut[kind][k4], host_lut(k4 ? 4 : 3, kind), nm, cudaMemcpyHostToDevice, s));
+        }
     const int64_t n = g->n, T = g->ntasks;
     char *fh = nullptr, *fl = nullptr, *ft = nullptr;
     int64_t *nsel = nullptr;
+    unsigned long long *ctr = nullptr;
     VDMC_CUDA(dalloc((void **)&fh, std::max<int64_t>(n, 1), s));
     VDMC_CUDA(dalloc((void **)&fl, std::max<int64_t>(n, 1), s));
     VDMC_CUDA(dalloc((void **)&ft, std::max<int64_t>(T, 1), s));
     VDMC_CUDA(dalloc((void **)&nsel, sizeof(int64_t) * 2, s));
-    if (!g->light_root) VDMC_CUDA(dalloc((void **)&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
-    if (!g->heavy_task) VDMC_CUDA(dalloc((void **)&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1), s));
+    VDMC_CUDA(dalloc((void **)&ctr, sizeof(unsigned long long) * 2, s));
+    VDMC_CUDA(dalloc((void **)&g->light_root, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(dalloc((void **)&g->heavy_task, sizeof(int32_t) * std::max<int64_t>(T, 1), s));
+    VDMC_CUDA(dalloc((void **)&g->hroots, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
+    VDMC_CUDA(dalloc((void **)&g->hbase, sizeof(int64_t) * std::max<int64_t>(n, 1), s));
     int64_t hn[2] = {0, 0};
+    int64_t nhr = 0;
     if (n > 0 && T > 0) {
         k_root_flags<<<148 * 8, 256, 0, s>>>(n, g->off, g->tfirst, fh, fl);
         VDMC_LAUNCH();
         k_task_flags<<<148 * 8, 256, 0, s>>>(T, g->task_root, fh, ft);
         VDMC_LAUNCH();
         thrust::counting_iterator<int32_t> ids(0);
-        size_t tb = 0, tb2 = 0;
+        size_t tb = 0, tb2 = 0, tb3 = 0;
         VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
+        VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb3, ids, fh, g->hroots, nsel, (int)n, s));
         void *ts = nullptr;
-        VDMC_CUDA(dalloc((void **)&ts, std::max(tb, tb2), s));
+        VDMC_CUDA(dalloc((void **)&ts, std::max(tb, std::max(tb2, tb3)), s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, ft, g->heavy_task, nsel, (int)T, s));
         VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb2, ids, fl, g->light_root, nsel + 1, (int)n, s));
-        count_launch(2);
         VDMC_CUDA(cudaMemcpyAsync(hn, nsel, sizeof hn, cudaMemcpyDeviceToHost, s));
-        dfree(ts, s);
-    }
-    // heavy roots (rank order) and the induced adjacency of each one's N+(r)
-    int64_t nhr = 0;
-    if (!g->hroots) VDMC_CUDA(dalloc((void **)&g->hroots, sizeof(int32_t) * std::max<int64_t>(n, 1), s));
-    if (!g->hbase) VDMC_CUDA(dalloc((void **)&g->hbase, sizeof(int64_t) * std::max<int64_t>(n, 1), s));
-    if (n > 0 && T > 0) {
-        thrust::counting_iterator<int32_t> ids(0);
-        size_t tb = 0;
-        VDMC_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids, fh, g->hroots, nsel, (int)n, s));
-        void *ts = nullptr;
-        VDMC_CUDA(dalloc((void **)&ts, tb, s));
-        VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb, ids, fh, g->hroots, nsel, (int)n, s));
-        count_launch(1);
+        VDMC_CUDA(cub::DeviceSelect::Flagged(ts, tb3, ids, fh, g->hroots, nsel, (int)n, s));
         VDMC_CUDA(cudaMemcpyAsync(&nhr, nsel, sizeof nhr, cudaMemcpyDeviceToHost, s));
+        count_launch(3);
         VDMC_CUDA(cudaStreamSynchronize(s));
         dfree(ts, s);
     }
+    g->nheavy = hn[0];
+    g->nlight = hn[1];
     g->nhroots = nhr;
     if (nhr > 0) {
         int64_t *dlist = nullptr, *segs = nullptr;
@@ -1404,7 +1458,7 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         void *ts = nullptr;
         VDMC_CUDA(dalloc((void **)&ts, tb, s));
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts, tb, dlist, segs, (int)(nhr + 1), s));
-        count_launch(2);
+        count_launch(1);
         k_scatter_hbase<<<148 * 4, 256, 0, s>>>(nhr, g->hroots, segs, g->hbase);
         VDMC_LAUNCH();
         int64_t sumD = 0;
@@ -1415,28 +1469,26 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
         int64_t *cnt = nullptr;
         VDMC_CUDA(dalloc((void **)&cnt, sizeof(int64_t) * (sumD + 1), s));
         VDMC_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (sumD + 1), s));
-        dfree(g->nr_off, s);
         VDMC_CUDA(dalloc((void **)&g->nr_off, sizeof(int64_t) * (sumD + 1), s));
         const int cap = (int)std::min<int64_t>(g->max_degree, 12288);
         const size_t sm = (size_t)std::max(cap, 1) * 4;
         VDMC_CUDA(cudaFuncSetAttribute(k_nr<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         VDMC_CUDA(cudaFuncSetAttribute(k_nr<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        VDMC_CUDA(cudaMemsetAsync(g->ctr + 2, 0, 2 * sizeof(unsigned long long), s));
+        VDMC_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
         k_nr<false><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, cnt, nullptr,
-                                            nullptr, g->ctr + 2, cap);
+                                            nullptr, ctr, cap);
         VDMC_LAUNCH();
         size_t tb2 = 0;
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
         void *ts2 = nullptr;
         VDMC_CUDA(dalloc((void **)&ts2, tb2, s));
         VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts2, tb2, cnt, g->nr_off, (int)(sumD + 1), s));
-        count_launch(2);
+        count_launch(1);
         VDMC_CUDA(cudaMemcpyAsync(&g->nr_total, g->nr_off + sumD, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         VDMC_CUDA(cudaStreamSynchronize(s));
-        dfree(g->nr_adj, s);
         VDMC_CUDA(dalloc((void **)&g->nr_adj, sizeof(uint32_t) * std::max<int64_t>(g->nr_total, 1), s));
         k_nr<true><<<148 * 2, 512, sm, s>>>(g->off, g->split, g->adj, g->hroots, nhr, g->hbase, nullptr, g->nr_off,
-                                           g->nr_adj, g->ctr + 3, cap);
+                                           g->nr_adj, ctr + 1, cap);
         VDMC_LAUNCH();
         dfree(ts2, s);
         dfree(cnt, s);
@@ -1447,73 +1499,75 @@ static vdmc_status ensure_roots(vdmc_graph *g, cudaStream_t s) {
     dfree(fl, s);
     dfree(ft, s);
     dfree(nsel, s);
-    VDMC_CUDA(cudaStreamSynchronize(s));
-    g->nheavy = hn[0];
-    g->nlight = hn[1];
-    g->roots_ready = 1;
+    dfree(ctr, s);
     return VDMC_OK;
 }
 
-vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t s) {
-    if (g->cost && g->cost_k == k) return VDMC_OK;
-    if (!g->cost) VDMC_CUDA(dalloc((void **)&g->cost, sizeof(int64_t) * std::max<int64_t>(g->ntasks, 1), s));
-    if (g->ntasks > 0) {
-        int64_t *raw = nullptr;
-        VDMC_CUDA(dalloc((void **)&raw, sizeof(int64_t) * g->ntasks, s));
-        k_cost<<<148 * 8, 256, 0, s>>>(g->ntasks, k, g->off, g->split, g->adj, g->tfirst, g->task_root, raw);
-        VDMC_LAUNCH();
-        size_t tb = 0;
-        VDMC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, raw, g->cost, (int)g->ntasks, s));
-        void *ts = nullptr;
-        VDMC_CUDA(dalloc((void **)&ts, tb, s));
-        VDMC_CUDA(cub::DeviceScan::InclusiveSum(ts, tb, raw, g->cost, (int)g->ntasks, s));
-        count_launch(2);
-        dfree(ts, s);
-        dfree(raw, s);
-        VDMC_CUDA(cudaStreamSynchronize(s));
-    }
-    g->cost_k = k;
+vdmc_status plan_prefix(const vdmc_graph *g, int k, int64_t *prefix_host, cudaStream_t s) {
+    if (g->ntasks <= 0) return VDMC_OK;
+    int64_t *raw = nullptr, *pre = nullptr;
+    VDMC_CUDA(dalloc((void **)&raw, sizeof(int64_t) * g->ntasks, s));
+    VDMC_CUDA(dalloc((void **)&pre, sizeof(int64_t) * g->ntasks, s));
+    k_cost<<<148 * 8, 256, 0, s>>>(g->ntasks, k, g->off, g->split, g->adj, g->tfirst, g->task_root, raw);
+    VDMC_LAUNCH();
+    size_t tb = 0;
+    VDMC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, raw, pre, (int)g->ntasks, s));
+    void *ts = nullptr;
+    VDMC_CUDA(dalloc((void **)&ts, tb, s));
+    VDMC_CUDA(cub::DeviceScan::InclusiveSum(ts, tb, raw, pre, (int)g->ntasks, s));
+    count_launch(1);
+    VDMC_CUDA(cudaMemcpyAsync(prefix_host, pre, sizeof(int64_t) * g->ntasks, cudaMemcpyDeviceToHost, s));
+    VDMC_CUDA(cudaStreamSynchronize(s));
+    dfree(ts, s);
+    dfree(raw, s);
+    dfree(pre, s);
     return VDMC_OK;
 }
+
+namespace {
+struct Events {   // per-call timing events (only when the caller asks for timings)
+    cudaEvent_t e[4] = {};
+    ~Events() {
+        for (auto x : e)
+            if (x) cudaEventDestroy(x);
+    }
+};
+}  // namespace
 
 template <int K, int C>
-static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int64_t lo, int64_t hi,
-                       cudaStream_t s) {
+static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts &o, unsigned long long *acc,
+                       int64_t lo, int64_t hi, cudaStream_t s, float *ms3) {
     const int dev = g->device;
     int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if (g->max_degree >= (int64_t(1) << 21))   // star3_heavy packs per-lane counts in 21-bit fields
+    if (g->max_degree >= (int64_t(1) << 21))
         return fail(VDMC_EINVAL, "max degree %lld >= 2^21 is not supported", (long long)g->max_degree);
-    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[0], s));
-    vdmc_status st = ensure_roots(g, s);
-    if (st) return st;
-    trace("ensure_roots");
+    Events ev;
+    if (ms3)
+        for (auto &x : ev.e) VDMC_CUDA(cudaEventCreate(&x));
+    if (ms3) VDMC_CUDA(cudaEventRecord(ev.e[0], s));
     bool heavy_in_smem = true;
     int64_t per_cta = 0;
-    // VDMC_HEAVY_GLOBAL=1 forces the global-memory fallback for heavy-task buffers (tests)
-    const char *force = getenv("VDMC_HEAVY_GLOBAL");
-    const Layout L = make_layout((int)g->max_degree, C, heavy_in_smem, per_cta, force && force[0] == '1');
+    const Layout L = make_layout((int)g->max_degree, C, heavy_in_smem, per_cta, o.heavy_global != 0);
     const size_t smem = (size_t)L.total * 4;
     auto kern = heavy_in_smem ? k_enum<K, C, true> : k_enum<K, C, false>;
     VDMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     VDMC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem));
     const int grid = std::max(1, nsm * std::max(per_sm, 1));
-    // global fallback scratch: heavy per-CTA buffers (huge degrees), light per-warp oversize L_a
+    // per-call scratch: heavy per-CTA buffers (global fallback), light per-warp oversize L_a,
+    // per-CTA CA lists of the cross items; work counters
     const int64_t per_warp = (int64_t)g->max_degree + (g->max_degree + 15) / 16 + 1;
-    const uint32_t ca_cap = 1u << 16;
+    const uint32_t ca_cap = o.ca_capacity > 0 ? (uint32_t)o.ca_capacity : (1u << 16);
     const int64_t per_cta_ca = 2 * (int64_t)std::max<int64_t>(g->max_degree, 1) + ca_cap;
     const size_t need = (size_t)grid * (per_cta + (int64_t)kWarps * per_warp + per_cta_ca);
-    if (g->lscratch_elems < need) {
-        dfree(g->lscratch, s);
-        g->lscratch = nullptr;
-        g->lscratch_elems = 0;
-        VDMC_CUDA(dalloc((void **)&g->lscratch, need * sizeof(uint32_t), s));
-        g->lscratch_elems = need;
-    }
-    VDMC_CUDA(cudaMemsetAsync(g->acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
-    VDMC_CUDA(cudaMemsetAsync(g->ctr, 0, 2 * sizeof(unsigned long long), s));
-    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[1], s));
+    uint32_t *scratch = nullptr;
+    unsigned long long *ctr = nullptr;
+    VDMC_CUDA(dalloc((void **)&scratch, need * sizeof(uint32_t), s));
+    VDMC_CUDA(dalloc((void **)&ctr, 2 * sizeof(unsigned long long), s));
+    VDMC_CUDA(cudaMemsetAsync(acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
+    VDMC_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+    if (ms3) VDMC_CUDA(cudaEventRecord(ev.e[1], s));
     trace("scratch+memset");
     Dev d{};
     d.off = g->off;
@@ -1525,67 +1579,79 @@ static vdmc_status run(vdmc_graph *g, const uint8_t *lut, uint64_t *counts, int6
     d.light_root = g->light_root;
     d.nheavy = g->nheavy;
     d.nlight = g->nlight;
-    // VDMC_PHASES (profiling only; results incomplete): 1 = heavy phase only, 2 = light only
-    if (const char *ph = getenv("VDMC_PHASES")) {
+#ifdef VDMC_PROFILING
+    // profiling build only (tools/): switches that drop work, results incomplete
+    if (const char *ph = getenv("VDMC_PHASES")) {   // 1 = heavy phase only, 2 = light only
         if (ph[0] == '1') d.nlight = 0;
         if (ph[0] == '2') d.nheavy = 0;
     }
-    if (const char *sk = getenv("VDMC_SKIP")) {   // profiling only; results incomplete
-        d.skip = atoi(sk);
-    }
-    if (const char *mr = getenv("VDMC_MINREM")) {   // profiling only; results incomplete
-        d.minrem = atoi(mr);
-    }
-    d.fold = kMaxBlock;
-    d.xblock = kCrossBlock;
-    if (const char *xb = getenv("VDMC_XBLOCK")) {   // tuning: cross-item block length
-        d.xblock = std::max(32, std::min(kMaxBlock, atoi(xb)));
-    }
-    if (const char *fo = getenv("VDMC_FOLD")) {   // tests: exercise the fold path on small graphs
-        d.fold = std::max(1, std::min(kMaxBlock, atoi(fo)));
-    }
-    d.acc = (unsigned long long *)g->acc;
+    if (const char *sk = getenv("VDMC_SKIP")) d.skip = atoi(sk);
+    if (const char *mr = getenv("VDMC_MINREM")) d.minrem = atoi(mr);
+#endif
+    d.fold = o.star_block > 0 ? o.star_block : kMaxBlock;
+    d.xblock = o.cross_block > 0 ? o.cross_block : kCrossBlock;
+    d.acc = acc;
     d.ns = (uint32_t)std::max<int64_t>(g->n, 1);
-    d.gheavy = g->lscratch;
-    d.glight = g->lscratch + (size_t)grid * per_cta;
-    d.gca = g->lscratch + (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
+    d.gheavy = scratch;
+    d.glight = scratch + (size_t)grid * per_cta;
+    d.gca = scratch + (size_t)grid * (per_cta + (int64_t)kWarps * per_warp);
     d.gca_per_cta = per_cta_ca;
     d.ca_cap = ca_cap;
     d.gheavy_per_cta = per_cta;
     d.glight_per_warp = per_warp;
     d.heavy_in_smem = heavy_in_smem ? 1 : 0;
-    d.big = g->max_degree > 32767 ? 1 : 0;
+    d.big = (g->max_degree > 32767 || o.force_big) ? 1 : 0;
     d.maxdeg = (int)g->max_degree;
     d.off32 = (uint64_t)std::max<int64_t>(g->n, 1) * C < (1ull << 32) ? 1 : 0;
     d.hbase = g->hbase;
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
     if (hi > lo) {
-        kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, g->ctr, lut);
+        kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, ctr, lut);
         VDMC_LAUNCH();
     }
-    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[2], s));
-    if (g->n > 0) {
-        const unsigned fg = (unsigned)std::min<int64_t>((g->n + kFinV - 1) / kFinV, (int64_t)nsm * 8);
-        k_finalize<C><<<fg, 256, 0, s>>>(g->n, g->order, (const unsigned long long *)g->acc,
-                                           (unsigned long long *)counts);
-        VDMC_LAUNCH();
+    if (ms3) VDMC_CUDA(cudaEventRecord(ev.e[2], s));
+    dfree(scratch, s);
+    dfree(ctr, s);
+    if (ms3) {
+        VDMC_CUDA(cudaEventSynchronize(ev.e[2]));
+        VDMC_CUDA(cudaEventElapsedTime(&ms3[0], ev.e[0], ev.e[1]));
+        VDMC_CUDA(cudaEventElapsedTime(&ms3[1], ev.e[1], ev.e[2]));
     }
-    if (g->profiling) VDMC_CUDA(cudaEventRecord(g->ev[3], s));
-    trace("enum+finalize enqueued");
+    trace("enum enqueued");
     return VDMC_OK;
 }
 
-vdmc_status launch_count(vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
-                         cudaStream_t s) {
-    trace("count start");
-    vdmc_status st = ensure_acc(g, k, kind, s);
-    if (st) return st;
-    trace("ensure_acc");
-    const uint8_t *lut = g->lut[kind][k == 4 ? 1 : 0];
-    if (kind == VDMC_UNDIRECTED)
-        return k == 3 ? run<3, kNumClassesU3>(g, lut, counts, lo, hi, s) : run<4, kNumClassesU4>(g, lut, counts, lo, hi, s);
-    return k == 3 ? run<3, kNumClasses3>(g, lut, counts, lo, hi, s) : run<4, kNumClasses4>(g, lut, counts, lo, hi, s);
+vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned long long *acc, int64_t lo,
+                       int64_t hi, cudaStream_t s, float *ms3) {
+    const uint8_t *lut = g->lut[o.kind][k == 4 ? 1 : 0];
+    if (o.kind == VDMC_UNDIRECTED)
+        return k == 3 ? run<3, kNumClassesU3>(g, lut, o, acc, lo, hi, s, ms3)
+                      : run<4, kNumClassesU4>(g, lut, o, acc, lo, hi, s, ms3);
+    return k == 3 ? run<3, kNumClasses3>(g, lut, o, acc, lo, hi, s, ms3)
+                  : run<4, kNumClasses4>(g, lut, o, acc, lo, hi, s, ms3);
+}
+
+template <int C>
+static void launch_finalize(int64_t n, const int32_t *order, const unsigned long long *acc, uint64_t *counts, int nsm,
+                            cudaStream_t s) {
+    const unsigned fg = (unsigned)std::min<int64_t>((n + kFinV - 1) / kFinV, (int64_t)nsm * 8);
+    k_finalize<C><<<fg, 256, 0, s>>>(n, order, acc, (unsigned long long *)counts);
+}
+
+vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, uint64_t *counts, cudaStream_t s) {
+    if (g->n <= 0) return VDMC_OK;
+    int nsm = 0;
+    VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    switch (C) {
+        case kNumClasses3: launch_finalize<kNumClasses3>(g->n, g->order, acc, counts, nsm, s); break;
+        case kNumClasses4: launch_finalize<kNumClasses4>(g->n, g->order, acc, counts, nsm, s); break;
+        case kNumClassesU3: launch_finalize<kNumClassesU3>(g->n, g->order, acc, counts, nsm, s); break;
+        case kNumClassesU4: launch_finalize<kNumClassesU4>(g->n, g->order, acc, counts, nsm, s); break;
+        default: return fail(VDMC_EINVAL, "no finalize for C=%d", C);
+    }
+    VDMC_LAUNCH();
+    return VDMC_OK;
 }
 
 }  // namespace vdmc

@@ -62,6 +62,8 @@ int num_classes(int k, int kind);
 }  // namespace vdmc
 
 // ------------------------------------------------------------ graph handle
+// Immutable once vdmc_build_graph* returns: count calls read it and draw their working memory
+// (accumulator, work counters, scratch) per call.
 struct vdmc_graph {
     int device = 0;
     int64_t n = 0, nnz = 0, arcs = 0, ntasks = 0, max_degree = 0;
@@ -73,20 +75,12 @@ struct vdmc_graph {
     int32_t *order = nullptr;      // [n]   order[rank] = original id
     int64_t *tfirst = nullptr;     // [n+1] first task of each root (exclusive scan of forward degrees)
     int32_t *task_root = nullptr;  // [ntasks]
-    // scratch owned by the handle (lazily grown)
-    uint64_t *acc = nullptr;       // [n][C] accumulator in rank order
-    size_t acc_bytes = 0;
-    uint32_t *lscratch = nullptr;  // per-warp depth-2 candidate lists
-    size_t lscratch_elems = 0;
-    unsigned long long *ctr = nullptr;   // work counter(s)
-    uint8_t *lut[2][2] = {};        // [kind][k == 4] device class LUTs
-    int64_t *cost = nullptr;       // [ntasks] inclusive prefix of the plan's cost proxy
-    int cost_k = 0;
-    // schedule: tasks of heavy roots (CTA per task) and light roots (warp per root), rank order
+    uint8_t *lut[2][2] = {};       // [kind][k == 4] device class LUTs (S3)
+    // S4 schedule: tasks of heavy roots (CTA per task) and light roots (warp per root), both
+    // ascending (= rank order, longest first), so a task slice maps to a contiguous sub-list
     int32_t *heavy_task = nullptr; // [nheavy]
     int32_t *light_root = nullptr; // [nlight]
     int64_t nheavy = 0, nlight = 0;
-    int roots_ready = 0;
     // induced adjacency of N+(r) in position space for heavy roots r (S4 pre-pass):
     // entries of the position p of root r: nr_adj[nr_off[hbase[r] + p] .. nr_off[hbase[r] + p + 1])
     int32_t *hroots = nullptr;     // [nhroots] heavy roots, rank order
@@ -95,18 +89,28 @@ struct vdmc_graph {
     int64_t *nr_off = nullptr;     // [sum D+ over heavy roots + 1]
     uint32_t *nr_adj = nullptr;    // position << 2 | code(x, R[position])
     int64_t nr_total = 0;
-    // profiling
-    int profiling = 0;
-    cudaEvent_t ev[8] = {};
-    float last_ms[5] = {0, 0, 0, 0, 0};
     float build_ms = 0;
 };
 
 namespace vdmc {
+struct CountOpts {   // validated vdmc_count_options
+    int kind = 0, star_block = 0, cross_block = 0, heavy_global = 0, force_big = 0;
+    int64_t ca_capacity = 0;
+    float *timings_ms = nullptr;
+};
 vdmc_status build_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst,
                          const int32_t *h_rank, int device, cudaStream_t stream, vdmc_graph *g);
-vdmc_status ensure_acc(vdmc_graph *g, int k, int kind, cudaStream_t s);
-vdmc_status ensure_plan(vdmc_graph *g, int k, cudaStream_t stream);
-vdmc_status launch_count(vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
-                         cudaStream_t stream);
+// S4 schedule + class LUT upload, run at the end of a build
+vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s);
+// per-task cost proxy, inclusive prefix (host [ntasks])
+vdmc_status plan_prefix(const vdmc_graph *g, int k, int64_t *prefix_host, cudaStream_t s);
+// count the slice [lo, hi) into the class-major accumulator acc [C][n] (caller-allocated
+// device memory, rank order); no finalise
+vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned long long *acc, int64_t lo,
+                       int64_t hi, cudaStream_t s, float *ms3);
+// class-major rank-order accumulator -> row-major [original id][C]
+vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, uint64_t *counts, cudaStream_t s);
+// S1 only, for vdmc_symmetrize: G_U entries in ORIGINAL ids, sorted by (owner, nbr), OR-merged
+vdmc_status symmetrize_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, cudaStream_t s,
+                              int64_t *nnz_out, uint64_t **d_entries, int *vb_out);
 }  // namespace vdmc

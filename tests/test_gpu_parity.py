@@ -24,7 +24,7 @@ def vd():
     return vdmc
 
 
-def gpu_count(vd, g, k, rank=None, device_edges=True):
+def gpu_count(vd, g, k, rank=None, device_edges=True, options=None):
     import torch
     n, s, d = g
     if device_edges:
@@ -32,7 +32,7 @@ def gpu_count(vd, g, k, rank=None, device_edges=True):
                       torch.from_numpy(np.ascontiguousarray(d, np.int32)).cuda(), rank=rank)
     else:
         gr = vd.Graph(n, s, d, rank=rank)
-    out = gr.count(k).cpu().numpy().view(np.uint64)
+    out = gr.count(k, options=options).cpu().numpy().view(np.uint64)
     gr.close()
     return out
 
@@ -88,21 +88,70 @@ def test_rank_invariance(vd, oracle_mod, k):
         assert np.array_equal(gpu_count(vd, g, k, rank=rank), want)
 
 
+PATH_MODES = {   # result-preserving path options (vdmc_count_options) forced on a small graph
+    "smem": {}, "random-rank": {},
+    "global": {"heavy_global": 1},                  # heavy buffers in global memory
+    "fold": {"star_block": 37},                     # star items of 37 b positions (default 1023)
+    "xblock": {"cross_block": 32},                  # "2+1" cross items of 32 positions (default 256)
+    "big": {"force_big": 1},                        # per-item histogram flushes (max degree > 32767)
+    "ca0": {"ca_capacity": 1},                      # every heavy task: per-c "2+1" fallback items
+    "all": {"heavy_global": 1, "star_block": 5, "cross_block": 33, "force_big": 1, "ca_capacity": 7},
+}
+
+
 @pytest.mark.parametrize("k", [3, 4])
-@pytest.mark.parametrize("mode", ["smem", "global", "random-rank", "fold"])
-def test_heavy_and_light_paths(vd, oracle_mod, k, mode, monkeypatch):
-    """A graph with roots on both sides of the light/heavy threshold (G_U degree 256): heavy
-    tasks with buffers in shared memory, forced into the global-memory fallback, and a random
-    vertex order (light roots next to long lists: the oversize-L_a fallback)."""
+@pytest.mark.parametrize("mode", sorted(PATH_MODES))
+def test_heavy_and_light_paths(vd, oracle_mod, k, mode):
+    """A graph with roots on both sides of the light/heavy threshold (G_U degree 128): heavy
+    tasks in every forced path, and a random vertex order (light roots next to long lists:
+    the oversize-L_a fallback)."""
     g = G.make_config("cfg3", scale=0.03)
     deg = np.bincount(np.concatenate([g[1], g[2]]), minlength=g[0])
     assert deg.max() > 300
-    if mode == "global":
-        monkeypatch.setenv("VDMC_HEAVY_GLOBAL", "1")
-    if mode == "fold":   # star chunks fold their 16-bit counters every 37 b's instead of 65535
-        monkeypatch.setenv("VDMC_FOLD", "37")
     rank = np.random.default_rng(3).permutation(g[0]) if mode == "random-rank" else None
-    assert np.array_equal(gpu_count(vd, g, k, rank=rank), oracle_mod.count_esu(g, k))
+    assert np.array_equal(gpu_count(vd, g, k, rank=rank, options=PATH_MODES[mode]), oracle_mod.count_esu(g, k))
+
+
+def _ca_needs(g):
+    """Per heavy task (r, x) under the default order (G_U degree descending, ties by id): the
+    CA entries its cross items need, sum over c in L_x of |N(c) n N+(r) \\ {x}|.  Host-side,
+    test-only arithmetic on the input graph (no method arithmetic)."""
+    n, s, d = g
+    a = np.concatenate([s, d]).astype(np.int64)
+    b = np.concatenate([d, s]).astype(np.int64)
+    key = np.unique(a * n + b)
+    u, v = key // n, key % n
+    deg = np.bincount(u, minlength=n)
+    order = np.lexsort((np.arange(n), -deg))
+    rank = np.empty(n, np.int64)
+    rank[order] = np.arange(n)
+    nb = [set() for _ in range(n)]
+    for x, y in zip(rank[u].tolist(), rank[v].tolist()):
+        nb[x].add(y)
+    needs = []
+    for r in range(n):
+        if len(nb[r]) <= 128:
+            continue
+        R = {y for y in nb[r] if y > r}
+        for x in R:
+            La = [c for c in nb[x] if c > r and c not in nb[r]]
+            needs.append(sum(len(nb[c] & R) - (1 if x in nb[c] else 0) for c in La))
+    return np.array(needs)
+
+
+@pytest.mark.parametrize("k", [4])
+def test_ca_overflow_mixed(vd, oracle_mod, k):
+    """ca_capacity at the median need: within one heavy root some tasks run the cross items and
+    others the per-c fallback; both keep the same partition of the "2+1" sets (a set belongs
+    to the task of the depth-1 vertex c hangs off first), so nothing is counted twice or
+    missed."""
+    g = G.make_config("cfg3", scale=0.03)
+    needs = _ca_needs(g)
+    cap = int(np.median(needs[needs > 0]))
+    assert (needs > cap).sum() > 10 and ((needs > 0) & (needs <= cap)).sum() > 10
+    want = oracle_mod.count_esu(g, k)
+    for c in (cap, max(1, cap // 4)):
+        assert np.array_equal(gpu_count(vd, g, k, options={"ca_capacity": c}), want), c
 
 
 @pytest.mark.parametrize("k", [3, 4])

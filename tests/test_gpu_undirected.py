@@ -21,12 +21,12 @@ def vd():
     return vdmc
 
 
-def ucount(vd, g, k, rank=None, work=None):
+def ucount(vd, g, k, rank=None, options=None):
     import torch
     n, s, d = g
     gr = vd.Graph(n, torch.from_numpy(np.ascontiguousarray(s, np.int32)).cuda(),
                   torch.from_numpy(np.ascontiguousarray(d, np.int32)).cuda(), rank=rank)
-    out = gr.count(k, kind="undirected").cpu().numpy().view(np.uint64)
+    out = gr.count(k, kind="undirected", options=options).cpu().numpy().view(np.uint64)
     gr.close()
     return out
 
@@ -44,13 +44,13 @@ def test_small_fixtures(vd, oracle_mod, k):
 
 
 @pytest.mark.parametrize("k", [3, 4])
-@pytest.mark.parametrize("mode", ["smem", "global", "random-rank"])
-def test_heavy_and_light_paths(vd, oracle_mod, k, mode, monkeypatch):
+@pytest.mark.parametrize("mode", ["smem", "global", "random-rank", "all"])
+def test_heavy_and_light_paths(vd, oracle_mod, k, mode):
     g = G.make_config("cfg3", scale=0.03)
-    if mode == "global":
-        monkeypatch.setenv("VDMC_HEAVY_GLOBAL", "1")
+    opts = {"global": {"heavy_global": 1},
+            "all": {"star_block": 5, "cross_block": 33, "force_big": 1, "ca_capacity": 7}}.get(mode)
     rank = np.random.default_rng(5).permutation(g[0]) if mode == "random-rank" else None
-    assert np.array_equal(ucount(vd, g, k, rank=rank), oracle_mod.count_undirected(g, k))
+    assert np.array_equal(ucount(vd, g, k, rank=rank, options=opts), oracle_mod.count_undirected(g, k))
 
 
 def test_slices_sum_to_full(vd):

@@ -1,4 +1,4 @@
-"""N > 1 host logic on CPU (gloo, world size 2): vdmc.count_distributed slices the task list
+"""N > 1 host logic on CPU (gloo, world size 2): vdmc.count_slices_reduce slices the task list
 with the planner's cost-balanced split, counts each slice into a private partial and
 reduces to rank 0.  The graph object is duck-typed: plan()/count() are served by the oracle
 over root ranges (the counting itself is the GPU's job and is covered by -m gpu), so this
@@ -43,7 +43,7 @@ def _worker(rank, world, port, k, q):
         g = G.make_config("cfg3", scale=0.004)
         sg = OracleSliceGraph(g, k)
         parts = sg.plan(k, world)
-        out = vdmc.count_distributed(sg, k)
+        out = vdmc.count_slices_reduce(sg, k)
         if rank == 0:
             q.put((parts, out.numpy().view(np.uint64).copy()))
     finally:

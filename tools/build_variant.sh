@@ -1,12 +1,15 @@
 #!/bin/bash
-# build an experimental libvdmc variant: tools/build_variant.sh NAME 'sed-expression-on-enum.cu'
+# build an experimental libvdmc variant (profiling build: -DVDMC_PROFILING):
+#   tools/build_variant.sh NAME 'sed-expression-on-enum.cu'
 set -e
 NAME=$1; EXPR=$2
 D=/tmp/vdmc_variant_$NAME; rm -rf $D; mkdir -p $D/csrc
 cp paper_2201_11655_b200/csrc/*.cu paper_2201_11655_b200/csrc/*.cuh $D/csrc/
 sed -i "$EXPR" $D/csrc/enum.cu
 sed -i 's#"../../include/vdmc.h"#"/root/repo/include/vdmc.h"#' $D/csrc/vdmc_internal.cuh
-F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr"
+NCCL=$(python -c "import paper_2201_11655_b200.build as b; print(b.NCCL)")
+F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -DVDMC_PROFILING -I$NCCL/include"
 for f in api build enum; do nvcc $F -c -o $D/$f.o $D/csrc/$f.cu & done; wait
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_2201_11655_b200/lib/libvdmc_$NAME.so $D/*.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_2201_11655_b200/lib/libvdmc_$NAME.so $D/*.o \
+    -L$NCCL/lib -l:libnccl.so.2 -Xlinker -rpath=$NCCL/lib
 echo built paper_2201_11655_b200/lib/libvdmc_$NAME.so

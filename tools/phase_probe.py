@@ -1,9 +1,13 @@
-"""Time k_enum with phases / loop kinds switched off (profiling only, results incomplete):
-python tools/phase_probe.py cfg4 [k] [quick]"""
+"""Time k_enum with phases / loop kinds switched off (profiling build libvdmc_prof.so only,
+results incomplete):  python tools/phase_probe.py cfg4 [k] [quick|tasks]"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2201_11655_b200 import build as B  # noqa: E402
+
+if "VDMC_LIB" not in os.environ:   # the switches below exist only in the profiling build (A/B variants are one)
+    os.environ["VDMC_LIB"] = B.build_profiling()
 import torch  # noqa: E402
 
 import graphgen as G  # noqa: E402
@@ -13,7 +17,6 @@ name = sys.argv[1]
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 n, s, d = G.make_config(name)
 g = vdmc.Graph(n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
-g.set_profiling(True)
 variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {"VDMC_PHASES": "2"}),
             ("skip star3_heavy", {"VDMC_SKIP": "1"}), ("skip b in R", {"VDMC_SKIP": "2"}),
             ("skip b in L_a", {"VDMC_SKIP": "4"}), ("heavy, skip star", {"VDMC_PHASES": "1", "VDMC_SKIP": "1"}),
@@ -22,10 +25,9 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("heavy, skip all", {"VDMC_PHASES": "1", "VDMC_SKIP": "7"}),
             ("no cross items (fallback)", {"VDMC_SKIP": "8"}),
             ("heavy, skip all, no ca_build", {"VDMC_PHASES": "1", "VDMC_SKIP": "15"}),
-            ("xblock 256", {"VDMC_XBLOCK": "256"}),
-            ("xblock 1023", {"VDMC_XBLOCK": "1023"}),
-            ("star block 512", {"VDMC_FOLD": "512"}), ("star block 256", {"VDMC_FOLD": "256"}),
-            ("star 512 xblock 256", {"VDMC_FOLD": "512", "VDMC_XBLOCK": "256"}),
+            ("xblock 128", {"cross_block": 128}),
+            ("xblock 1023", {"cross_block": 1023}),
+            ("star block 512", {"star_block": 512}), ("star block 256", {"star_block": 256}),
             ("heavy, only tasks with >= 128 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "128"}),
             ("heavy, only tasks with < 128 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "-128"}),
             ("heavy, only tasks with >= 512 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "512"}),
@@ -35,13 +37,14 @@ if len(sys.argv) > 3 and sys.argv[3] == "quick":
 elif len(sys.argv) > 3 and sys.argv[3] == "tasks":
     variants = variants[:2] + [v for v in variants if "VDMC_MINREM" in v[1]]
 for label, env in variants:
-    for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_XBLOCK", "VDMC_FOLD", "VDMC_MINREM"):
+    for key in ("VDMC_PHASES", "VDMC_SKIP", "VDMC_MINREM"):
         os.environ.pop(key, None)
-    os.environ.update(env)
+    opts = {key: v for key, v in env.items() if not key.startswith("VDMC_")}
+    os.environ.update({key: v for key, v in env.items() if key.startswith("VDMC_")})
     ts = []
     for _ in range(3):
-        out = g.count(k)
-        torch.cuda.synchronize()
-        ts.append(g.timings()["enum"])
+        t = {}
+        out = g.count(k, options=opts, timings=t)
+        ts.append(t["enum"])
         del out
     print(f"{name} k={k} {label:24s} enum {min(ts):8.2f} ms", flush=True)

@@ -1,5 +1,5 @@
 """Run one BASELINE config's count a few times (for ncu / quick timing):
-python tools/profile_enum.py cfg3 4 [reps] [scale]"""
+python tools/profile_enum.py cfg3 4 [reps] [scale] [kind]"""
 import os
 import sys
 
@@ -12,12 +12,12 @@ from paper_2201_11655_b200 import vdmc  # noqa: E402
 name, k = sys.argv[1], int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 scale = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
+kind = sys.argv[5] if len(sys.argv) > 5 else "directed"
 n, s, d = G.make_config(name, scale=scale)
 g = vdmc.Graph(n, torch.from_numpy(s).cuda(), torch.from_numpy(d).cuda())
-g.set_profiling(True)
 for _ in range(reps):
-    out = g.count(k)
+    t = {}
+    out = g.count(k, kind=kind, timings=t)
     torch.cuda.synchronize()
-t = g.timings()
-print(f"{name} k={k} enum_ms={t['enum']:.2f} plan_ms={t['plan']:.2f} build_ms={t['build']:.2f} "
+print(f"{name} k={k} {kind} enum_ms={t['enum']:.2f} schedule_ms={t['schedule']:.2f} build_ms={g.info['build_ms']:.2f} "
       f"sets={int(out.sum().item()) // k}", flush=True)

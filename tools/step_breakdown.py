@@ -21,16 +21,15 @@ for it in range(reps):
     g = vdmc.Graph(n, ds, dd)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    g.set_profiling(True)
-    out = g.count(k)
+    tm = {}
+    out = g.count(k, timings=tm)
     t2 = time.perf_counter()
     torch.cuda.synchronize()
     t3 = time.perf_counter()
-    tm = g.timings()
     g.close()
     torch.cuda.synchronize()
     t4 = time.perf_counter()
     del out
-    print(f"{name} k={k} rep {it}: build {1e3*(t1-t0):.1f} ms (events {tm['build']:.1f}); count host-return "
-          f"{1e3*(t2-t1):.1f} ms, done {1e3*(t3-t1):.1f} ms (plan {tm['plan']:.1f} enum {tm['enum']:.1f} "
+    print(f"{name} k={k} rep {it}: build {1e3*(t1-t0):.1f} ms (events {g.info['build_ms']:.1f}); count host-return "
+          f"{1e3*(t2-t1):.1f} ms, done {1e3*(t3-t1):.1f} ms (schedule {tm['schedule']:.1f} enum {tm['enum']:.1f} "
           f"finalize {tm['finalize']:.1f}); close {1e3*(t4-t3):.1f} ms", flush=True)
