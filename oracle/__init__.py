@@ -25,6 +25,11 @@ Contents (each function cites the PAPER.md passage it follows; see
 * ``count_py_undirected`` — pure-Python brute force for undirected motifs, classes named by
                        (edge count, degree sequence) (shares nothing with the C file).
 * ``expected_gnp_undirected`` — Eq. 4 with the undirected n_max = C(k, 2).
+* ``edge_list`` / ``count_edges_brute`` / ``count_edges_esu`` — edge-level counts, the
+                       Discussion's extension ("counting motifs for edges ... only requires
+                       updating edges and not vertices"): +1 in the set's class for every G_U
+                       edge inside the set; rows = G_U edges {u < v} in lexicographic order.
+* ``count_edges_py`` — pure-Python brute force of the same (tiny graphs; shares nothing with C).
 
 Every function is pinned by ``tests/test_oracle_*.py`` (closed forms, the
 hand-worked golden of the paper's example graph, single-motif graphs,
@@ -327,3 +332,68 @@ def expected_gnp_undirected(k: int, n: int, p: float) -> np.ndarray:
     iso = n_iso_undirected(k)
     nmax = k * (k - 1) // 2
     return math.comb(n - 1, k - 1) * iso * p ** ne * (1.0 - p) ** (nmax - ne)
+
+
+# ------------------------------------------------------------------ edge-level counts
+def edge_list(g):
+    """G_U edges (u < v), lexicographic: the row order of every edge-level matrix."""
+    lib = _load()
+    n, s, d = _edges(g)
+    ne = ctypes.c_int64(0)
+    _check(lib.oracle_edge_list(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d), None, None,
+                                ctypes.byref(ne)))
+    eu = np.zeros(max(ne.value, 1), np.int32)
+    ev = np.zeros(max(ne.value, 1), np.int32)
+    _check(lib.oracle_edge_list(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d), _p(eu), _p(ev),
+                                ctypes.byref(ne)))
+    return eu[: ne.value].copy(), ev[: ne.value].copy()
+
+
+def count_edges_brute(g, k: int) -> np.ndarray:
+    """[edges][C]: the definition over all C(n, k) subsets, every G_U edge of each connected set."""
+    lib = _load()
+    n, s, d = _edges(g)
+    ne = edge_list(g)[0].size
+    out = np.zeros((ne, num_classes(k)), np.uint64)
+    _check(lib.oracle_count_edges_brute(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d),
+                                        ctypes.c_int(k), _p(out)))
+    return out
+
+
+def count_edges_esu(g, k: int, root_lo: int = 0, root_hi: int | None = None, threads: int = 0) -> np.ndarray:
+    """[edges][C] via ESU (sets whose minimum original id is in [root_lo, root_hi))."""
+    lib = _load()
+    n, s, d = _edges(g)
+    if root_hi is None:
+        root_hi = n
+    ne = edge_list(g)[0].size
+    out = np.zeros((ne, num_classes(k)), np.uint64)
+    _check(lib.oracle_count_edges_esu(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d), ctypes.c_int(k),
+                                      ctypes.c_int64(root_lo), ctypes.c_int64(root_hi), ctypes.c_int(threads),
+                                      _p(out)))
+    return out
+
+
+def count_edges_py(g, k: int):
+    """Pure-Python brute force, tiny graphs: {((u, v), canonical id): count} with u < v."""
+    n, s, d = g
+    arcs = set(zip(s.tolist(), d.tolist()))
+    out: dict = {}
+    for S in itertools.combinations(range(n), k):
+        und = {(x, y) for x in S for y in S if x < y and ((x, y) in arcs or (y, x) in arcs)}
+        comp = {S[0]}
+        grew = True
+        while grew:
+            grew = False
+            for (x, y) in und:
+                if (x in comp) != (y in comp):
+                    comp |= {x, y}
+                    grew = True
+        if len(comp) < k:
+            continue
+        best = min(paper_index(k, {(i, j) for i in range(k) for j in range(k)
+                                   if i != j and (P[i], P[j]) in arcs})
+                   for P in itertools.permutations(S))
+        for e in und:
+            out[(e, best)] = out.get((e, best), 0) + 1
+    return out

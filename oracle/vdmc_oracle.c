@@ -24,6 +24,11 @@
  *   oracle_count_vertex per-vertex rows for sampled vertices (ESU with v forced minimal)
  *   oracle_count_bfs    the paper's own method: proper k-BFS(i) per root, BFS depth
  *                       labels, Lemma 3 rules + Lemma 4 correction
+ *   oracle_edge_list, oracle_count_edges_brute, oracle_count_edges_esu
+ *                       edge-level counts, the Discussion's extension ("counting motifs for
+ *                       edges, rather than vertices ... only requires updating edges and not
+ *                       vertices once a motif was counted"): for every connected k-set S and every
+ *                       G_U edge {x, y} inside S, ecounts[row(x, y)][col] += 1 (reading G18)
  *
  * Pins: tests/test_oracle_*.py (brute force vs closed forms, hand-worked golden,
  * single-motif graphs, invariants, Eq. 4).  No function here is "parity unpinned".
@@ -231,6 +236,48 @@ static void add_set(uint64_t *counts, int nc, int k, const int32_t *v, int col) 
     }
 }
 
+/* ----------------------------------------------------- edge-level counts */
+/* Edge rows: the G_U edges {x < y} in lexicographic order, i.e. the upper entries of the
+ * undirected CSR read row by row.  erow[e] = row of the pair of CSR entry e (both
+ * entries of a pair get the same row). */
+static int64_t *edge_rows(const ograph *g, int64_t *nedges) {
+    int64_t nnz = g->uind[g->n];
+    int64_t *erow = malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int64_t));
+    if (!erow) return NULL;
+    int64_t row = 0;
+    for (int32_t x = 0; x < g->n; x++)
+        for (int64_t e = g->uind[x]; e < g->uind[x + 1]; e++)
+            if (g->unbr[e] > x) erow[e] = row++;
+    for (int32_t x = 0; x < g->n; x++)
+        for (int64_t e = g->uind[x]; e < g->uind[x + 1]; e++) {
+            int32_t y = g->unbr[e];
+            if (y > x) continue;
+            /* the mirror entry x in y's list */
+            int64_t lo = g->uind[y], hi = g->uind[y + 1];
+            while (lo < hi) { int64_t mid = (lo + hi) / 2; if (g->unbr[mid] < x) lo = mid + 1; else hi = mid; }
+            erow[e] = erow[lo];
+        }
+    *nedges = row;
+    return erow;
+}
+
+static int64_t edge_row(const ograph *g, const int64_t *erow, int32_t x, int32_t y) {
+    int64_t lo = g->uind[x], hi = g->uind[x + 1];
+    while (lo < hi) { int64_t mid = (lo + hi) / 2; if (g->unbr[mid] < y) lo = mid + 1; else hi = mid; }
+    return erow[lo];
+}
+
+/* +1 in that class for every G_U edge of the set ("updating edges and not vertices") */
+static void add_set_edges(const ograph *g, const int64_t *erow, uint64_t *ecounts, int nc, int k,
+                          const int32_t *v, int col) {
+    for (int a = 0; a < k; a++)
+        for (int b = a + 1; b < k; b++)
+            if (adjacent(g, v[a], v[b])) {
+                #pragma omp atomic
+                ecounts[edge_row(g, erow, v[a], v[b]) * nc + col] += 1;
+            }
+}
+
 /* ================================================================ exports */
 
 /* The paper's CSR for a directed edge list: directed out-lists and G_U lists. */
@@ -311,6 +358,7 @@ int oracle_count_brute(int64_t n, int64_t m, const int32_t *src, const int32_t *
  * Per-thread state: nsub[u] = |N(u) n Vsub| (u in N(Vsub) iff nsub[u] > 0), insub[u]. */
 typedef struct {
     const ograph *g; const otable *t; uint64_t *counts;
+    uint64_t *ecounts; const int64_t *erow;  /* edge-level mode: per G_U edge, else NULL */
     int k; int32_t root; int root_is_min;   /* root_is_min: every other vertex is "> root" */
     int32_t *nsub; uint8_t *insub;
     int32_t sub[MAXK];
@@ -328,7 +376,10 @@ static void esu_pop(esu_ctx *c, int32_t w) {
 
 static void esu_extend(esu_ctx *c, int s, int32_t *ext, int64_t next) {
     if (s == c->k) {
-        add_set(c->counts, c->t->nclasses, c->k, c->sub, classify(c->g, c->t, c->sub));
+        if (c->ecounts)
+            add_set_edges(c->g, c->erow, c->ecounts, c->t->nclasses, c->k, c->sub, classify(c->g, c->t, c->sub));
+        else
+            add_set(c->counts, c->t->nclasses, c->k, c->sub, classify(c->g, c->t, c->sub));
         c->nsets++;
         return;
     }
@@ -574,5 +625,99 @@ int oracle_count_bfs(int64_t n, int64_t m, const int32_t *src, const int32_t *ds
     }
     free(idx); free(byidx);
     free_table(&t); free_graph(&g);
+    return 0;
+}
+
+/* ------------------------------------------------------ edge-level exports */
+/* The G_U edge rows: eu[r] < ev[r], lexicographic.  eu/ev may be NULL (count only). */
+int oracle_edge_list(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                     int32_t *eu, int32_t *ev, int64_t *nedges) {
+    ograph g;
+    int rc = make_graph(n, m, src, dst, &g);
+    if (rc) return rc;
+    int64_t row = 0;
+    for (int32_t x = 0; x < n; x++)
+        for (int64_t e = g.uind[x]; e < g.uind[x + 1]; e++)
+            if (g.unbr[e] > x) {
+                if (eu) eu[row] = x;
+                if (ev) ev[row] = g.unbr[e];
+                row++;
+            }
+    *nedges = row;
+    free_graph(&g);
+    return 0;
+}
+
+/* Definition written out for edges: every k-subset connected in G_U, +1 in its class for every
+ * G_U edge inside it.  ecounts: [nedges][nclasses], rows as oracle_edge_list. */
+int oracle_count_edges_brute(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                             int k, uint64_t *ecounts) {
+    otable t; ograph g;
+    if (k != 3 && k != 4) return -1;
+    int rc = make_graph(n, m, src, dst, &g);
+    if (rc) return rc;
+    if ((rc = make_table(k, &t))) { free_graph(&g); return rc; }
+    int64_t ne = 0;
+    int64_t *erow = edge_rows(&g, &ne);
+    if (!erow) { free_table(&t); free_graph(&g); return -4; }
+    memset(ecounts, 0, (size_t)ne * t.nclasses * sizeof(uint64_t));
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i0 = 0; i0 < n; i0++) {
+        int64_t c[MAXK];
+        c[0] = i0;
+        for (int a = 1; a < k; a++) c[a] = i0 + a;
+        if (c[k - 1] >= n) continue;
+        for (;;) {
+            int32_t v[MAXK];
+            for (int a = 0; a < k; a++) v[a] = (int32_t)c[a];
+            int par[MAXK];
+            for (int a = 0; a < k; a++) par[a] = a;
+            for (int a = 0; a < k; a++)
+                for (int b = a + 1; b < k; b++)
+                    if (adjacent(&g, v[a], v[b])) par[uf_find(par, a)] = uf_find(par, b);
+            int ok = 1;
+            for (int a = 1; a < k; a++) if (uf_find(par, a) != uf_find(par, 0)) ok = 0;
+            if (ok) add_set_edges(&g, erow, ecounts, t.nclasses, k, v, classify(&g, &t, v));
+            int a = k - 1;
+            while (a >= 1 && c[a] == n - k + a) a--;
+            if (a < 1) break;
+            c[a]++;
+            for (int b = a + 1; b < k; b++) c[b] = c[b - 1] + 1;
+        }
+    }
+    free(erow); free_table(&t); free_graph(&g);
+    return 0;
+}
+
+/* The same via ESU (every connected k-set once, from its minimum id in [root_lo, root_hi)). */
+int oracle_count_edges_esu(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int k,
+                           int64_t root_lo, int64_t root_hi, int nthreads, uint64_t *ecounts) {
+    otable t; ograph g;
+    if (k != 3 && k != 4) return -1;
+    if (root_lo < 0) root_lo = 0;
+    if (root_hi > n) root_hi = n;
+    int rc = make_graph(n, m, src, dst, &g);
+    if (rc) return rc;
+    if ((rc = make_table(k, &t))) { free_graph(&g); return rc; }
+    int64_t ne = 0;
+    int64_t *erow = edge_rows(&g, &ne);
+    if (!erow) { free_table(&t); free_graph(&g); return -4; }
+    memset(ecounts, 0, (size_t)ne * t.nclasses * sizeof(uint64_t));
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    #pragma omp parallel
+    {
+        esu_ctx c;
+        memset(&c, 0, sizeof(c));
+        c.g = &g; c.t = &t; c.ecounts = ecounts; c.erow = erow; c.k = k;
+        c.nsub = calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+        c.insub = calloc((size_t)(n > 0 ? n : 1), 1);
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t r = root_lo; r < root_hi; r++) {
+            c.root = (int32_t)r; c.root_is_min = 0;
+            esu_root(&c);
+        }
+        free(c.nsub); free(c.insub);
+    }
+    free(erow); free_table(&t); free_graph(&g);
     return 0;
 }
