@@ -167,6 +167,23 @@ vdmc_status vdmc_count_kind(const vdmc_graph *g, int k, int kind, uint64_t *coun
 vdmc_status vdmc_count_ex(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
                           const vdmc_count_options *opt, void *stream);
 
+/* Edge-level counts, the Discussion's extension: "counting motifs for
+ * edges, rather than vertices ... only requires updating edges and not vertices once a motif
+ * was counted".
+ *   counts[e][j] = number of connected k-sets S containing both ends of the G_U edge e whose
+ *                  class is vdmc_class_ids_kind(k, kind)[j]  (every G_U edge inside S: +1)
+ * counts: device uint64 [ntasks][C] (one row per G_U edge; ntasks = edges), rows in the
+ * canonical edge order: (u, v) with u < v ORIGINAL ids, lexicographic (vdmc_get_edges lists
+ * them).  work / opt / stream as vdmc_count_ex (only opt->kind and opt->timings_ms are used: the
+ * edge path enumerates every set explicitly).  Partials of disjoint task slices sum to the full
+ * result.  Errors: as vdmc_count_ex, plus VDMC_EINVAL for >= 2^31 edges. */
+vdmc_status vdmc_count_edges(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
+                             const vdmc_count_options *opt, void *stream);
+
+/* The G_U edge of each row of vdmc_count_edges: u[e] < v[e], original ids, lexicographic
+ * (host int32 [ntasks] each; synchronous).  Errors: VDMC_EINVAL, VDMC_ECUDA. */
+vdmc_status vdmc_get_edges(const vdmc_graph *g, int32_t *u, int32_t *v);
+
 /* Cost-balanced split of the task list into nparts contiguous slices:
  * parts[p] for p in [0, nparts).  Uses a per-task cost proxy of the kernels' work computed on
  * the device (synchronous; nothing is cached in the graph).

@@ -545,6 +545,25 @@ vdmc_status vdmc_count(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_
     return vdmc_count_ex(g, k, counts, work, nullptr, stream);
 }
 
+vdmc_status vdmc_count_edges(const vdmc_graph *g, int k, uint64_t *counts, const vdmc_range *work,
+                             const vdmc_count_options *opt, void *stream) {
+    CountOpts o;
+    vdmc_status st = check_opts(k, opt, o);
+    if (st) return st;
+    if (!g) return fail(VDMC_EINVAL, "graph is NULL");
+    if (!counts && g->ntasks > 0) return fail(VDMC_EINVAL, "counts is NULL");
+    int64_t lo, hi;
+    if ((st = check_work(g, work, lo, hi))) return st;
+    VDMC_CUDA(cudaSetDevice(g->device));
+    return count_edges_impl(g, k, o.kind, counts, lo, hi, (cudaStream_t)stream, o.timings_ms);
+}
+
+vdmc_status vdmc_get_edges(const vdmc_graph *g, int32_t *u, int32_t *v) {
+    if (!g || ((!u || !v) && g->ntasks > 0)) return fail(VDMC_EINVAL, "NULL argument");
+    VDMC_CUDA(cudaSetDevice(g->device));
+    return edge_list_impl(g, u, v);
+}
+
 vdmc_status vdmc_root_range(const vdmc_graph *g, int64_t pos_lo, int64_t pos_hi, vdmc_range *out) {
     if (!g || !out) return fail(VDMC_EINVAL, "NULL argument");
     if (pos_lo < 0 || pos_hi < pos_lo || pos_hi > g->n)

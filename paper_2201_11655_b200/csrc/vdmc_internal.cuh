@@ -110,6 +110,11 @@ vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned 
                        int64_t hi, cudaStream_t s, float *ms3);
 // class-major rank-order accumulator -> row-major [original id][C]
 vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, uint64_t *counts, cudaStream_t s);
+// edge-level counts (edges.cu): counts [edges][C] in the canonical edge order; ms (optional,
+// host float[4]) as vdmc_count_options.timings_ms
+vdmc_status count_edges_impl(const vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
+                             cudaStream_t s, float *ms);
+vdmc_status edge_list_impl(const vdmc_graph *g, int32_t *u, int32_t *v);
 // S1 only, for vdmc_symmetrize: G_U entries in ORIGINAL ids, sorted by (owner, nbr), OR-merged
 vdmc_status symmetrize_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, cudaStream_t s,
                               int64_t *nnz_out, uint64_t **d_entries, int *vb_out);

@@ -20,7 +20,7 @@ STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASY
 
 # Every symbol include/vdmc.h declares (tests check the .so exports exactly these)
 EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_symmetrize", "vdmc_free_host", "vdmc_count",
-           "vdmc_count_kind", "vdmc_count_ex", "vdmc_plan", "vdmc_split_costs", "vdmc_root_range",
+           "vdmc_count_kind", "vdmc_count_ex", "vdmc_count_edges", "vdmc_get_edges", "vdmc_plan", "vdmc_split_costs", "vdmc_root_range",
            "vdmc_num_classes", "vdmc_class_ids", "vdmc_num_classes_kind", "vdmc_class_ids_kind",
            "vdmc_get_info", "vdmc_get_order", "vdmc_kernel_launches", "vdmc_comm_unique_id",
            "vdmc_comm_init", "vdmc_comm_free", "vdmc_count_distributed", "vdmc_free_graph", "vdmc_trim",
@@ -79,6 +79,9 @@ def lib():
             "vdmc_count_ex": (_i32, [_vp, ctypes.c_int, _vp, ctypes.POINTER(Range), ctypes.POINTER(CountOptions),
                                      _vp]),
             "vdmc_root_range": (_i32, [_vp, _i64, _i64, ctypes.POINTER(Range)]),
+            "vdmc_count_edges": (_i32, [_vp, ctypes.c_int, _vp, ctypes.POINTER(Range),
+                                        ctypes.POINTER(CountOptions), _vp]),
+            "vdmc_get_edges": (_i32, [_vp, _vp, _vp]),
             "vdmc_comm_unique_id": (_i32, [_vp]),
             "vdmc_comm_init": (_i32, [ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.POINTER(_vp)]),
             "vdmc_comm_free": (None, [_vp]),
@@ -282,6 +285,40 @@ class Graph:
         if timings is not None:
             timings.update(zip(["schedule", "enum", "finalize", "count"], list(buf)))
         return out
+
+    def count_edges(self, k: int, out=None, work=None, stream=None, kind="directed", timings=None):
+        """Edge-level counts: uint64 [edges][C] as an int64 tensor on
+        the graph's device; rows in the order of edges() (u < v original ids, lexicographic)."""
+        import torch
+        kd = _kind(kind)
+        C = num_classes(k, kd)
+        o, buf = _options(kd, None, timings)
+        if C < 0:
+            _check(lib().vdmc_count_edges(self._h, k, None, None, ctypes.byref(o), None))
+        E = self.ntasks
+        if out is None:
+            out = torch.empty((E, C), dtype=torch.int64, device=f"cuda:{self.device}")
+        if not (out.is_cuda and out.device.index == self.device and out.dtype == torch.int64
+                and out.is_contiguous() and tuple(out.shape) == (E, C)):
+            raise ValueError(f"out must be a contiguous int64 [{E}, {C}] tensor on cuda:{self.device}")
+        rng = None if work is None else Range(int(work[0]), int(work[1]))
+        with torch.cuda.device(self.device):
+            _check(lib().vdmc_count_edges(self._h, k, out.data_ptr() if out.numel() else None,
+                                          ctypes.byref(rng) if rng is not None else None, ctypes.byref(o),
+                                          _stream_ptr(stream)))
+        if timings is not None:
+            timings.update(zip(["schedule", "enum", "finalize", "count"], list(buf)))
+        return out
+
+    def edges(self):
+        """(u, v) original ids of each edge row of count_edges (u < v, lexicographic)."""
+        E = self.ntasks
+        u = np.zeros(max(E, 1), np.int32)
+        v = np.zeros(max(E, 1), np.int32)
+        with_dev = __import__("torch").cuda.device(self.device)
+        with with_dev:
+            _check(lib().vdmc_get_edges(self._h, u.ctypes.data, v.ctypes.data))
+        return u[:E], v[:E]
 
     def plan(self, k: int, nparts: int):
         parts = (Range * nparts)()
