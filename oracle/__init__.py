@@ -29,6 +29,7 @@ Contents (each function cites the PAPER.md passage it follows; see
                        Discussion's extension ("counting motifs for edges ... only requires
                        updating edges and not vertices"): +1 in the set's class for every G_U
                        edge inside the set; rows = G_U edges {u < v} in lexicographic order.
+* ``count_edge_rows`` — rows of sampled edges (per-edge ESU), for full-size sampled parity.
 * ``count_edges_py`` — pure-Python brute force of the same (tiny graphs; shares nothing with C).
 
 Every function is pinned by ``tests/test_oracle_*.py`` (closed forms, the
@@ -371,6 +372,19 @@ def count_edges_esu(g, k: int, root_lo: int = 0, root_hi: int | None = None, thr
     _check(lib.oracle_count_edges_esu(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d), ctypes.c_int(k),
                                       ctypes.c_int64(root_lo), ctypes.c_int64(root_hi), ctypes.c_int(threads),
                                       _p(out)))
+    return out
+
+
+def count_edge_rows(g, k: int, eu, ev, threads: int = 0) -> np.ndarray:
+    """Rows of sampled G_U edges {eu[i], ev[i]} of count_edges_* (per-edge ESU: every set containing
+    eu[i], kept if it contains ev[i])."""
+    lib = _load()
+    n, s, d = _edges(g)
+    eu = np.ascontiguousarray(eu, dtype=np.int32)
+    ev = np.ascontiguousarray(ev, dtype=np.int32)
+    out = np.zeros((eu.size, num_classes(k)), np.uint64)
+    _check(lib.oracle_count_edge_rows(ctypes.c_int64(n), ctypes.c_int64(s.size), _p(s), _p(d), ctypes.c_int(k),
+                                      ctypes.c_int64(eu.size), _p(eu), _p(ev), ctypes.c_int(threads), _p(out)))
     return out
 
 

@@ -359,6 +359,7 @@ int oracle_count_brute(int64_t n, int64_t m, const int32_t *src, const int32_t *
 typedef struct {
     const ograph *g; const otable *t; uint64_t *counts;
     uint64_t *ecounts; const int64_t *erow;  /* edge-level mode: per G_U edge, else NULL */
+    int32_t need; uint64_t *row;             /* edge-row mode: only sets containing `need`, into row */
     int k; int32_t root; int root_is_min;   /* root_is_min: every other vertex is "> root" */
     int32_t *nsub; uint8_t *insub;
     int32_t sub[MAXK];
@@ -376,7 +377,11 @@ static void esu_pop(esu_ctx *c, int32_t w) {
 
 static void esu_extend(esu_ctx *c, int s, int32_t *ext, int64_t next) {
     if (s == c->k) {
-        if (c->ecounts)
+        if (c->row) {   /* edge-row mode: the root is one end of the edge, `need` the other */
+            int has = 0;
+            for (int i = 0; i < c->k; i++) has |= c->sub[i] == c->need;
+            if (has) c->row[classify(c->g, c->t, c->sub)] += 1;
+        } else if (c->ecounts)
             add_set_edges(c->g, c->erow, c->ecounts, c->t->nclasses, c->k, c->sub, classify(c->g, c->t, c->sub));
         else
             add_set(c->counts, c->t->nclasses, c->k, c->sub, classify(c->g, c->t, c->sub));
@@ -719,5 +724,42 @@ int oracle_count_edges_esu(int64_t n, int64_t m, const int32_t *src, const int32
         free(c.nsub); free(c.insub);
     }
     free(erow); free_table(&t); free_graph(&g);
+    return 0;
+}
+
+/* Rows of sampled edges {eu[i], ev[i]} (must be G_U edges): every connected k-set containing
+ * both ends, per class -- ESU from eu[i] with eu[i] treated as the minimum (every set containing
+ * it, once), keeping the sets that contain ev[i].  rows: [ne][nclasses]. */
+int oracle_count_edge_rows(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int k,
+                           int64_t ne, const int32_t *eu, const int32_t *ev, int nthreads, uint64_t *rows) {
+    otable t; ograph g;
+    if (k != 3 && k != 4) return -1;
+    for (int64_t i = 0; i < ne; i++)
+        if (eu[i] < 0 || eu[i] >= n || ev[i] < 0 || ev[i] >= n) return -2;
+    int rc = make_graph(n, m, src, dst, &g);
+    if (rc) return rc;
+    for (int64_t i = 0; i < ne; i++)
+        if (!adjacent(&g, eu[i], ev[i])) { free_graph(&g); return -1; }
+    if ((rc = make_table(k, &t))) { free_graph(&g); return rc; }
+    int nc = t.nclasses;
+    memset(rows, 0, (size_t)ne * nc * sizeof(uint64_t));
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    #pragma omp parallel
+    {
+        esu_ctx c;
+        memset(&c, 0, sizeof(c));
+        c.g = &g; c.t = &t; c.k = k;
+        c.nsub = calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+        c.insub = calloc((size_t)(n > 0 ? n : 1), 1);
+        #pragma omp for schedule(dynamic, 1)
+        for (int64_t i = 0; i < ne; i++) {
+            c.row = rows + i * nc;
+            c.need = ev[i];
+            c.root = eu[i]; c.root_is_min = 1;
+            esu_root(&c);
+        }
+        free(c.nsub); free(c.insub);
+    }
+    free_table(&t); free_graph(&g);
     return 0;
 }

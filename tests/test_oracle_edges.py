@@ -138,3 +138,14 @@ def test_root_range_partials(oracle_mod, k):
     for lo, hi in ((0, 5), (5, 100), (100, n)):
         acc += oracle_mod.count_edges_esu(g, k, lo, hi)
     assert np.array_equal(acc, full)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_edge_rows_match_full(oracle_mod, k):
+    """Per-edge rows (the full-size sampling oracle) equal the rows of the full matrix."""
+    g = G.make_config("cfg3", scale=0.002)
+    full = oracle_mod.count_edges_esu(g, k)
+    eu, ev = oracle_mod.edge_list(g)
+    pick = np.random.default_rng(k).choice(eu.size, 40, replace=False)
+    for a, b in ((eu, ev), (ev, eu)):   # either end may be the ESU root
+        assert np.array_equal(oracle_mod.count_edge_rows(g, k, a[pick], b[pick]), full[pick])
