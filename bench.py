@@ -423,8 +423,8 @@ def roofline(args, k, motifs, enum_ms, peak, peak_src):
     b_full = 4 + 16 * (k - 1)
     roof["B_k"] = b_full
     roof["frac_B_k"] = motifs * b_full / t / 1e9 / peak
-    if c:
-        atoms = c["l2_red_requests"] + c["l2_atom_requests"]
+    if c and "l2_red_requests" in c:
+        atoms = c["l2_red_requests"] + c.get("l2_atom_requests", 0)
         b_eff = 4 + 16 * atoms / motifs
         achieved = motifs * b_eff / t / 1e9
         roof.update({"achieved": achieved, "frac": achieved / peak, "B_k_eff": b_eff,

@@ -75,7 +75,8 @@ struct Dev {
     int big;                                  // flush the u32 histograms per item (degrees > 32767, or forced)
     int maxdeg;
     int off32;                                // n * C < 2^32: 32-bit accumulator offsets
-    int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields)
+    int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields);
+                                              // 0 = per task, sized so a task has ~2 items per warp
     int xblock;                               // cross items: positions per item (<= kMaxBlock)
 #ifdef VDMC_PROFILING
     int skip;                                 // profiling build only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
@@ -376,7 +377,7 @@ __device__ void build_a_cta(uint32_t r, List al, const uint32_t *R, int D, uint3
 //   * events (an a-b edge: every set of that b; a b-c edge: that c's set) are classified one
 //     by one through the LUT entry of their full mask (star_event).
 // Every set is counted once, in the class of its exact mask.  A work item is a chunk x a block
-// of at most g.fold (<= 65535: 16-bit fields) consecutive b positions: items of bounded length
+// of at most `fold` (<= 1023: 10-bit fields) consecutive b positions: items of bounded length
 // balance a task's warps; at a block's end the c's still ahead take U and every c flushes.
 // Counts are packed in 10-bit fields (inc_of), so a block spans at most kMaxBlock = 1023 b's.
 constexpr int kStarM = 4;                  // c slots per lane
@@ -543,7 +544,7 @@ __device__ __forceinline__ int next_a_event(const uint8_t *codes, int j, int jen
 }
 
 // star item (k, jb) of the task (r, a = R[i]): c positions [cb, ce) = [max(D - W(k+1), i+2), D - W k)
-// (chunk k), b positions [jlo, jhi) = block jb of [i+1, ce) in steps of g.fold
+// (chunk k), b positions [jlo, jhi) = block jb of [i+1, ce) in steps of fold
 __device__ __forceinline__ int star_blocks(int D, int i, int k, int S) {
     const int ce = D - kStarW * k;
     return (ce - i - 1 + S - 1) / S;
@@ -552,10 +553,10 @@ __device__ __forceinline__ int star_blocks(int D, int i, int k, int S) {
 template <int C>
 __device__ __forceinline__ void star_item(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                           int D, const uint32_t *Ba, const uint8_t *codes, uint32_t cra, uint32_t a,
-                                          uint32_t *H, int k, int jb, int lane) {
+                                          uint32_t *H, int k, int jb, int fold, int lane) {
     const int64_t seg = g.hbase[r];
     const int ce = D - kStarW * k, cb = max(ce - kStarW, i + 2);
-    const int jlo = i + 1 + jb * g.fold, jhi = min(ce, jlo + g.fold);
+    const int jlo = i + 1 + jb * fold, jhi = min(ce, jlo + fold);
     StarS s;
     s.keys = 0;
 #pragma unroll
@@ -1063,8 +1064,11 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(VDMC_SKIPF(g) & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
+        // b-block length: fixed (option), or per task so its ~nch * rem / 2 star iterations make
+        // about 2 items per warp (small tasks no longer leave most warps idle at the task barrier)
+        const int fold = g.fold > 0 ? g.fold : max(64, min(kMaxBlock, nch * (D - i - 1) / (4 * NW)));
         int nstar = 0;   // star items: chunk x block of b positions
-        for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, g.fold);
+        for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
         const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
         const int nB = cross ? nck * njb : nL;                                  // "2+1" items
         const int total = nstar + nB + nL;
@@ -1078,7 +1082,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             if (it < nstar) {
                 int rem = it, kk = 0;
                 for (;; kk++) {
-                    const int nb = star_blocks(D, i, kk, g.fold);
+                    const int nb = star_blocks(D, i, kk, fold);
                     if (rem < nb) break;
                     rem -= nb;
                 }
@@ -1088,7 +1092,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                 b_it = it - nstar;
             }
             if (star_k >= 0) {
-                if (!(VDMC_SKIPF(g) & 1)) star_item<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, star_b, lane);
+                if (!(VDMC_SKIPF(g) & 1)) star_item<C>(g, lut, r, i, R, D, Ba, codes, cra, a, H, star_k, star_b, fold, lane);
             } else if (b_it >= 0) {
                 if (VDMC_SKIPF(g) & 2) continue;
                 if (cross)
@@ -1588,7 +1592,7 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     if (const char *sk = getenv("VDMC_SKIP")) d.skip = atoi(sk);
     if (const char *mr = getenv("VDMC_MINREM")) d.minrem = atoi(mr);
 #endif
-    d.fold = o.star_block > 0 ? o.star_block : kMaxBlock;
+    d.fold = o.star_block;   // 0 = per-task block length
     d.xblock = o.cross_block > 0 ? o.cross_block : kCrossBlock;
     d.acc = acc;
     d.ns = (uint32_t)std::max<int64_t>(g->n, 1);

@@ -81,7 +81,7 @@ def test_cfg4_hub_roots_identity_order(vd, oracle_mod):
     for t in th:
         t.join()
     for r in roots:
-        assert got[r].sum(dtype=np.uint64) > 10 ** 9
+        assert got[r].sum(dtype=np.uint64) > 8 * 10 ** 8   # k x (sets rooted at r), about 4 x 2.5e8
         assert np.array_equal(got[r], want[r]), r
 
 
