@@ -105,7 +105,7 @@ def class_table(k: int) -> dict:
     canon = np.zeros(M, np.int32)
     conn = np.zeros(M, np.uint8)
     col = np.zeros(M, np.int32)
-    ids = np.zeros(256, np.int32)
+    ids = np.zeros(16384, np.int32)
     nc = ctypes.c_int32(0)
     _check(lib.oracle_class_table(ctypes.c_int(k), _p(canon), _p(conn), _p(col), _p(ids),
                                   ctypes.byref(nc)))

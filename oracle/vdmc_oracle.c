@@ -40,7 +40,8 @@
 #include <string.h>
 #include <omp.h>
 
-#define MAXK 4
+#define MAXK 5   /* k = 5: SURVEY §8(f) NEXT-3, "appropriate for 5 motifs too" */
+#define MAXCLASSES 16384
 
 /* ------------------------------------------------------------------ graph */
 typedef struct {
@@ -177,18 +178,19 @@ typedef struct {
     int32_t *canon;      /* [2^nbits] minimum index over all k! orders */
     uint8_t *conn;       /* [2^nbits] weakly connected? */
     int32_t *col;        /* [2^nbits] column of canon (ascending canonical ids), -1 if disconnected */
-    int32_t class_ids[256];
+    int32_t class_ids[MAXCLASSES];   /* 13 / 199 / 9364 for k = 3 / 4 / 5 */
 } otable;
 
 static int make_table(int k, otable *t) {
     memset(t, 0, sizeof(*t));
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     t->k = k; t->nbits = k * (k - 1);
     int M = 1 << t->nbits;
     t->canon = malloc((size_t)M * sizeof(int32_t));
     t->conn = malloc((size_t)M);
     t->col = malloc((size_t)M * sizeof(int32_t));
     if (!t->canon || !t->conn || !t->col) return -4;
+    #pragma omp parallel for schedule(static)
     for (int m = 0; m < M; m++) {
         int a[MAXK][MAXK], b[MAXK][MAXK], p[MAXK];
         matrix_of_index(k, m, a);
@@ -211,8 +213,9 @@ static int make_table(int k, otable *t) {
     for (int m = 0; m < M; m++) {
         t->col[m] = -1;
         if (!t->conn[m]) continue;
-        for (int c = 0; c < nc; c++)
-            if (t->class_ids[c] == t->canon[m]) { t->col[m] = c; break; }
+        int lo = 0, hi = nc;   /* class_ids ascending: binary search for canon[m] */
+        while (lo < hi) { int mid = (lo + hi) / 2; if (t->class_ids[mid] < t->canon[m]) lo = mid + 1; else hi = mid; }
+        t->col[m] = lo;
     }
     return 0;
 }
@@ -313,7 +316,7 @@ int oracle_class_table(int k, int32_t *canon, uint8_t *conn, int32_t *col,
 int oracle_count_brute(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                        int k, uint64_t *counts) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     int rc = make_graph(n, m, src, dst, &g);
     if (rc) return rc;
     if ((rc = make_table(k, &t))) { free_graph(&g); return rc; }
@@ -430,7 +433,7 @@ int oracle_count_esu(int64_t n, int64_t m, const int32_t *src, const int32_t *ds
                      int64_t root_lo, int64_t root_hi, int nthreads, uint64_t *counts,
                      uint64_t *nsets_out) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     if (root_lo < 0) root_lo = 0;
     if (root_hi > n) root_hi = n;
     int rc = make_graph(n, m, src, dst, &g);
@@ -464,7 +467,7 @@ int oracle_count_esu(int64_t n, int64_t m, const int32_t *src, const int32_t *ds
 int oracle_count_vertex(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int k,
                         int64_t nv, const int32_t *verts, int nthreads, uint64_t *rows) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     for (int64_t i = 0; i < nv; i++) if (verts[i] < 0 || verts[i] >= n) return -2;
     int rc = make_graph(n, m, src, dst, &g);
     if (rc) return rc;
@@ -658,7 +661,7 @@ int oracle_edge_list(int64_t n, int64_t m, const int32_t *src, const int32_t *ds
 int oracle_count_edges_brute(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
                              int k, uint64_t *ecounts) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     int rc = make_graph(n, m, src, dst, &g);
     if (rc) return rc;
     if ((rc = make_table(k, &t))) { free_graph(&g); return rc; }
@@ -698,7 +701,7 @@ int oracle_count_edges_brute(int64_t n, int64_t m, const int32_t *src, const int
 int oracle_count_edges_esu(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int k,
                            int64_t root_lo, int64_t root_hi, int nthreads, uint64_t *ecounts) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     if (root_lo < 0) root_lo = 0;
     if (root_hi > n) root_hi = n;
     int rc = make_graph(n, m, src, dst, &g);
@@ -733,7 +736,7 @@ int oracle_count_edges_esu(int64_t n, int64_t m, const int32_t *src, const int32
 int oracle_count_edge_rows(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int k,
                            int64_t ne, const int32_t *eu, const int32_t *ev, int nthreads, uint64_t *rows) {
     otable t; ograph g;
-    if (k != 3 && k != 4) return -1;
+    if (k < 3 || k > MAXK) return -1;
     for (int64_t i = 0; i < ne; i++)
         if (eu[i] < 0 || eu[i] >= n || ev[i] < 0 || ev[i] >= n) return -2;
     int rc = make_graph(n, m, src, dst, &g);
