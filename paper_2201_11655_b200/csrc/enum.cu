@@ -76,7 +76,7 @@ struct Dev {
     int maxdeg;
     int off32;                                // n * C < 2^32: 32-bit accumulator offsets
     int fold;                                 // star items: b positions per item (<= kMaxBlock: 10-bit fields);
-                                              // 0 = per task, sized so a task has ~2 items per warp
+                                              // 0 = default kMaxBlock
     int xblock;                               // cross items: positions per item (<= kMaxBlock)
 #ifdef VDMC_PROFILING
     int skip;                                 // profiling build only: bit0 star3_heavy, bit1 b in R loop, bit2 b in L_a loop, bit3 no cross items (ca_build)
@@ -1064,9 +1064,10 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(VDMC_SKIPF(g) & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
-        // b-block length: fixed (option), or per task so its ~nch * rem / 2 star iterations make
-        // about 2 items per warp (small tasks no longer leave most warps idle at the task barrier)
-        const int fold = g.fold > 0 ? g.fold : max(64, min(kMaxBlock, nch * (D - i - 1) / (4 * NW)));
+        // b-block length of the star items (option; default kMaxBlock)
+        // (measured: a per-task block of ~2 items per warp, min 64, is slower on cfg4, 470 vs 456 ms,
+        // gpurun_out/r02b/ab_fold_cfg4.txt: the per-item setup outweighs the tail it removes)
+        const int fold = g.fold > 0 ? g.fold : kMaxBlock;
         int nstar = 0;   // star items: chunk x block of b positions
         for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
         const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
