@@ -1279,10 +1279,42 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int32_t *__re
     }
 }
 
-// S4 cost proxy per task (r, a): sets of shape "3" plus the list lengths the other shapes scan
+// S4 cost model per task (r, a = R[i]), in picoseconds of whole-GPU time, fitted to the measured
+// phase times of the kernel as built (tools/plan_features.py + tools/phase_probe.py):
+//   heavy root (CTA per task): the star items count ~128 sets per warp iteration, so the task's
+//     cost is a per-task constant (phase A, CA lists, barriers) plus rem^2, rem = D - i - 1;
+//   light root (warp per root): per-task constant plus the explicit work W = sum_{j > i} deg(R[j])
+//     (b-in-R walks) + S2(a) (b-in-L_a walks) + rem^2 / 2 + rem * d_a + d_a^2 / 2 (the pair loops).
+// S2(v) = sum of the G_U degrees of v's neighbours; fsum = inclusive prefix over tasks of deg(R[i]).
+__global__ void k_s2(int64_t n, const int64_t *__restrict__ off, const uint32_t *__restrict__ adj,
+                     int64_t *__restrict__ s2) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; v < n;
+         v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t acc = 0;
+        for (int64_t q = off[v] + lane; q < off[v + 1]; q += 32) {
+            const uint32_t u = adj[q] >> 2;
+            acc += off[u + 1] - off[u];
+        }
+        for (int d = 16; d; d >>= 1) acc += __shfl_down_sync(kFull, acc, d);
+        if (lane == 0) s2[v] = acc;
+    }
+}
+
+__global__ void k_task_deg(int64_t ntasks, const int64_t *__restrict__ off, const int64_t *__restrict__ split,
+                           const uint32_t *__restrict__ adj, const int64_t *__restrict__ tfirst,
+                           const int32_t *__restrict__ task_root, int64_t *__restrict__ fdeg) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntasks; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = task_root[t];
+        const uint32_t a = adj[split[r] + (t - tfirst[r])] >> 2;
+        fdeg[t] = off[a + 1] - off[a];
+    }
+}
+
 __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, const int64_t *__restrict__ split,
                        const uint32_t *__restrict__ adj, const int64_t *__restrict__ tfirst,
-                       const int32_t *__restrict__ task_root, int64_t *__restrict__ cost) {
+                       const int32_t *__restrict__ task_root, const int64_t *__restrict__ s2,
+                       const int64_t *__restrict__ fsum, int64_t *__restrict__ cost) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntasks; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = task_root[t];
         const int64_t rs = split[r], re = off[r + 1];
@@ -1290,7 +1322,18 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
         const int64_t rem = re - ia - 1;
         const uint32_t a = adj[ia] >> 2;
         const int64_t da = off[a + 1] - off[a];
-        cost[t] = k == 3 ? 1 + rem + da : 1 + rem * (rem - 1) / 2 + rem * da + da * da;
+        const bool heavy = off[r + 1] - off[r] > kLightDeg;
+        int64_t c;
+        if (k == 3) {
+            c = heavy ? 112000 + 50 * (rem + da) : 5960 + 30 * (rem + da);
+        } else if (heavy) {
+            c = 112000 + rem * rem * 221 / 1000;
+        } else {
+            const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];   // sum_{j > i} deg(R[j])
+            const int64_t w = suf + s2[a] + rem * rem / 2 + rem * da + da * da / 2;
+            c = 5960 + w * 373 / 100;
+        }
+        cost[t] = c;
     }
 }
 
@@ -1510,17 +1553,27 @@ vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s) {
 
 vdmc_status plan_prefix(const vdmc_graph *g, int k, int64_t *prefix_host, cudaStream_t s) {
     if (g->ntasks <= 0) return VDMC_OK;
-    int64_t *raw = nullptr, *pre = nullptr;
+    int64_t *raw = nullptr, *pre = nullptr, *s2 = nullptr, *fsum = nullptr;
     VDMC_CUDA(dalloc((void **)&raw, sizeof(int64_t) * g->ntasks, s));
     VDMC_CUDA(dalloc((void **)&pre, sizeof(int64_t) * g->ntasks, s));
-    k_cost<<<148 * 8, 256, 0, s>>>(g->ntasks, k, g->off, g->split, g->adj, g->tfirst, g->task_root, raw);
-    VDMC_LAUNCH();
+    VDMC_CUDA(dalloc((void **)&s2, sizeof(int64_t) * std::max<int64_t>(g->n, 1), s));
+    VDMC_CUDA(dalloc((void **)&fsum, sizeof(int64_t) * g->ntasks, s));
     size_t tb = 0;
     VDMC_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, raw, pre, (int)g->ntasks, s));
     void *ts = nullptr;
     VDMC_CUDA(dalloc((void **)&ts, tb, s));
+    k_s2<<<148 * 16, 256, 0, s>>>(g->n, g->off, g->adj, s2);
+    VDMC_LAUNCH();
+    k_task_deg<<<148 * 8, 256, 0, s>>>(g->ntasks, g->off, g->split, g->adj, g->tfirst, g->task_root, raw);
+    VDMC_LAUNCH();
+    VDMC_CUDA(cub::DeviceScan::InclusiveSum(ts, tb, raw, fsum, (int)g->ntasks, s));
+    count_launch(1);
+    k_cost<<<148 * 8, 256, 0, s>>>(g->ntasks, k, g->off, g->split, g->adj, g->tfirst, g->task_root, s2, fsum, raw);
+    VDMC_LAUNCH();
     VDMC_CUDA(cub::DeviceScan::InclusiveSum(ts, tb, raw, pre, (int)g->ntasks, s));
     count_launch(1);
+    dfree(s2, s);
+    dfree(fsum, s);
     VDMC_CUDA(cudaMemcpyAsync(prefix_host, pre, sizeof(int64_t) * g->ntasks, cudaMemcpyDeviceToHost, s));
     VDMC_CUDA(cudaStreamSynchronize(s));
     dfree(ts, s);

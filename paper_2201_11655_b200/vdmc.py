@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("VDMC_LIB") or os.path.join(_HERE, "lib", "libvdmc.so")   # VDMC_LIB: A/B builds
+LIB_PATH = os.path.join(_HERE, "lib", "libvdmc.so")   # VDMC_LIB (read at first load) selects an A/B build
 
 VDMC_OK = 0
 STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASYM",
@@ -62,8 +62,9 @@ _i32 = ctypes.c_int32
 
 def lib():
     """Load libvdmc.so (built by __graft_entry__.build()); raise if it is missing."""
-    global _lib
+    global _lib, LIB_PATH
     if _lib is None:
+        LIB_PATH = os.environ.get("VDMC_LIB") or LIB_PATH
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"libvdmc.so not built ({LIB_PATH}); run __graft_entry__.build()")
         L = ctypes.CDLL(LIB_PATH)
