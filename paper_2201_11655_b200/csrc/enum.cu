@@ -1279,13 +1279,14 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int32_t *__re
     }
 }
 
-// S4 cost model per task (r, a = R[i]), in picoseconds of whole-GPU time, fitted to the measured
-// phase times of the kernel as built (tools/plan_features.py + tools/phase_probe.py):
-//   heavy root (CTA per task): the star items count ~128 sets per warp iteration, so the task's
-//     cost is a per-task constant (phase A, CA lists, barriers) plus rem^2, rem = D - i - 1;
-//   light root (warp per root): per-task constant plus the explicit work W = sum_{j > i} deg(R[j])
-//     (b-in-R walks) + S2(a) (b-in-L_a walks) + rem^2 / 2 + rem * d_a + d_a^2 / 2 (the pair loops).
-// S2(v) = sum of the G_U degrees of v's neighbours; fsum = inclusive prefix over tasks of deg(R[i]).
+// S4 cost model per task (r, a = R[i]), in picoseconds of whole-GPU time.  Terms:
+// rem = D - i - 1 (positions of R after a), nla = |{x in N(a): x > r}| (a's list beyond r: L_a
+// plus a's R-neighbours), D = |R|.  Coefficients: a non-negative least-squares fit of the
+// measured enumeration time of 32 planner slices and 3 phase totals on cfg4 and cfg5 (two
+// earlier models' slicings; tools/fit_plan.py, profiles/r02_planner_fit.txt; every row within 16 %):
+//   heavy root (CTA per task):  92.3 ns + 0.0915 ps rem^2 (star items) + 3.53 ps nla D (cross items)
+//   light root (warp per root): 1.45 ns + 12.8 ps rem nla + 49 ps nla^2 (pair loops and walks)
+// (k_s2 / k_task_deg feed the walk terms the fit found insignificant; kept for k = 3's model.)
 __global__ void k_s2(int64_t n, const int64_t *__restrict__ off, const uint32_t *__restrict__ adj,
                      int64_t *__restrict__ s2) {
     const int lane = threadIdx.x & 31;
@@ -1323,15 +1324,22 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
         const uint32_t a = adj[ia] >> 2;
         const int64_t da = off[a + 1] - off[a];
         const bool heavy = off[r + 1] - off[r] > kLightDeg;
+        int64_t lo = off[a], hi = off[a + 1];   // first entry of a's list with rank > r
+        const uint32_t key = ((uint32_t)r + 1u) << 2;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (adj[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        const int64_t nla = off[a + 1] - lo, D = re - rs;
         int64_t c;
         if (k == 3) {
-            c = heavy ? 112000 + 50 * (rem + da) : 5960 + 30 * (rem + da);
+            const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
+            c = heavy ? 92290 + 50 * (rem + da) : 1454 + 10 * (rem + nla) + suf + s2[a] / 8;
         } else if (heavy) {
-            c = 112000 + rem * rem * 221 / 1000;
+            c = 92290 + rem * rem * 9151 / 100000 + nla * D * 3528 / 1000;
         } else {
-            const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];   // sum_{j > i} deg(R[j])
-            const int64_t w = suf + s2[a] + rem * rem / 2 + rem * da + da * da / 2;
-            c = 5960 + w * 373 / 100;
+            c = 1454 + rem * nla * 1275 / 100 + nla * nla * 49;
         }
         cost[t] = c;
     }
