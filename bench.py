@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--edges", action="store_true",
+                   help="time edge-level counts (SURVEY 8(f) NEXT-2, vdmc_count_edges) instead of vertex counts")
     p.add_argument("--virtual-parts", type=int, default=0,
                    help="planner balance on one GPU: time each of G cost-balanced slices (vdmc_plan) back "
                         "to back and print max/mean (not the contract line)")
@@ -275,6 +277,11 @@ def main():
 
     def step(e_src, e_dst, out_host=None, tm=None):
         g = vdmc.Graph(n, e_src, e_dst, device=local)
+        if args.edges:
+            out = g.count_edges(k, kind=args.kind, timings=tm)
+            if out_host is not None:
+                out_host.copy_(out, non_blocking=True)
+            return g, out
         if world > 1:
             out = vdmc.count_distributed(g, k, comm, root=0, kind=args.kind)
         else:
@@ -285,7 +292,27 @@ def main():
 
     def motifs_of(out):
         colsum = out.sum(dim=0).cpu().numpy().view(np.uint64).astype(object)
+        if args.edges:   # sum over edges = sum over sets of their G_U edge count: checked, not divided
+            return edge_sum_to_motifs(colsum)
         return int(sum(colsum)) // k
+
+    edge_census = None
+    if args.edges:   # the motif count itself from one vertex count (outside any timed region)
+        if world > 1:
+            raise SystemExit("--edges runs on one GPU")
+        g0 = vdmc.Graph(n, d_src, d_dst, device=local)
+        vc = g0.count(k, kind=args.kind).sum(dim=0).cpu().numpy().view(np.uint64).astype(object)
+        g0.close()
+        ids = vdmc.class_ids(k, args.kind)
+        pairs = [(i, j) for i in range(k) for j in range(k) if i != j]
+        nb = len(pairs)
+        ecls = [len({tuple(sorted(pairs[b])) for b in range(nb) if (int(c) >> (nb - 1 - b)) & 1}) for c in ids]
+        edge_census = ([int(x) // k for x in vc], ecls)
+
+    def edge_sum_to_motifs(colsum):
+        census, ecls = edge_census
+        assert [int(x) for x in colsum] == [c * e for c, e in zip(census, ecls)], "edge census identity"
+        return sum(census)
 
     for _ in range(args.warmup):
         g, out = step(d_src, d_dst)
@@ -332,7 +359,12 @@ def main():
     h_src = torch.from_numpy(src).pin_memory()
     h_dst = torch.from_numpy(dst).pin_memory()
     C = vdmc.num_classes(k, args.kind)
-    h_out = torch.empty((n, C), dtype=torch.int64).pin_memory() if rank == 0 else None
+    rows = n
+    if args.edges:
+        g0 = vdmc.Graph(n, d_src, d_dst, device=local)
+        rows = g0.ntasks
+        g0.close()
+    h_out = torch.empty((rows, C), dtype=torch.int64).pin_memory() if rank == 0 else None
 
     def e2e_step():
         s_dev = h_src.to(dev, non_blocking=True)
@@ -380,12 +412,13 @@ def main():
                         "all": step_ms},
             "config": {"workload": f"{args.config}: {G.CONFIGS[args.config]['desc']}", "k": k, "n": n,
                        "arcs": arcs, "motif_kind": args.kind,
+                       "counts": "edge-level (NEXT-2)" if args.edges else "vertex-level",
                        "parallelism": f"dp{world} (graph replicated, cost-balanced task slices, ncclReduce)"
                        if world > 1 else "single GPU",
                        "l2": "flushed between steps (256 MiB write); count matrix >> L2"},
             "e2e": {"value": total_sets / (E_ms / 1e3), "unit": "motifs/s",
                     "h2d_bytes_per_step": int(2 * 4 * arcs),
-                    "d2h_bytes_per_step": int(n * C * 8), "ms_per_step": E_ms},
+                    "d2h_bytes_per_step": int(rows * C * 8), "ms_per_step": E_ms},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -397,6 +430,8 @@ def main():
                                  **{f"{key}_avg": statistics.mean(t[key] for t in phase_ms)
                                     for key in ("build", "schedule", "finalize")}}
             line["roofline"] = roofline(args, k, total_sets, enum_avg, peak, peak_src)
+            if args.edges:
+                line["roofline"]["kernel"] = f"k_edges<{k}>"
         if world == 1 and not args.no_cpu_baseline:
             rate, sets, dt, hi, cores = oracle_sample((n, src, dst), k, args.cpu_seconds)
             line["cpu_baseline"] = {"value": rate, "unit": "motifs/s", "cores": cores, "kind": "oracle",
@@ -417,7 +452,7 @@ def roofline(args, k, motifs, enum_ms, peak, peak_src):
     dram_frac: measured DRAM bytes per launch (ncu) over the live kernel time, vs the same peak.
     issue_frac: warp instructions issued / (SMSPs x cycles) in the ncu capture."""
     t = enum_ms / 1e3
-    c = ncu_counters(args.config, k, args.kind)
+    c = ncu_counters(args.config + ("-edges" if args.edges else ""), k, args.kind)
     roof = {"bound": "hbm", "kernel": f"k_enum<{k}>", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
             "motifs_per_launch": motifs}
     b_full = 4 + 16 * (k - 1)

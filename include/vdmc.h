@@ -90,6 +90,7 @@ typedef struct {
  *   ca_capacity  entries of the per-CTA scratch holding the R-neighbour lists of a heavy
  *                task's depth-2 vertices (default 65536); a task whose lists do not fit
  *                enumerates its "2+1" sets one depth-2 vertex at a time instead
+ *   layered      1 = the generic BFS-layer path (layers.cu; the only path for k = 5) for k = 3 / 4
  *   timings_ms   NULL, or host float[4] filled with device times (schedule + memset, enumerate,
  *                finalise, whole call); the call then synchronises `stream` before returning */
 typedef struct {
@@ -98,7 +99,7 @@ typedef struct {
     int32_t cross_block;
     int32_t heavy_global;
     int32_t force_big;
-    int32_t reserved0;
+    int32_t layered;
     int64_t ca_capacity;
     float *timings_ms;
 } vdmc_count_options;
@@ -146,7 +147,12 @@ vdmc_status vdmc_symmetrize(int64_t n, const int64_t *out_indptr, const int32_t 
 /* Release host memory returned by the library (vdmc_symmetrize).  NULL is a no-op. */
 void vdmc_free_host(void *p);
 
-/* Count k-motifs (k in {3,4}) into counts: device uint64 [n][vdmc_num_classes(k)], row =
+/* 5-vertex motifs ("appropriate for 5 motifs too"): vdmc_count /
+ * vdmc_count_kind / vdmc_count_ex accept k = 5 and run the generic BFS-layer path (one set per
+ * lane, 16-bit LUT of 2^20 masks); counts is then device uint64 [n][9364] (directed) or [n][21]
+ * (undirected).  k = 5 is not available in vdmc_count_edges / vdmc_count_distributed (VDMC_EK).
+ *
+ * Count k-motifs (k in {3,4}) into counts: device uint64 [n][vdmc_num_classes(k)], row =
  * original vertex id, fully overwritten.  work = NULL counts everything; otherwise only the
  * motifs whose (root, depth-1 neighbour) task lies in *work.  The partials of any set of
  * disjoint slices covering [0, ntasks) sum to the full result bit-exactly (integer adds).
@@ -200,7 +206,7 @@ vdmc_status vdmc_split_costs(const int64_t *prefix, int64_t ntasks, int nparts, 
  * Errors: VDMC_EINVAL (NULL, 0 <= pos_lo <= pos_hi <= n violated), VDMC_ECUDA. */
 vdmc_status vdmc_root_range(const vdmc_graph *g, int64_t pos_lo, int64_t pos_hi, vdmc_range *out);
 
-/* 13 for k = 3, 199 for k = 4, -1 otherwise. */
+/* 13 for k = 3, 199 for k = 4, 9364 for k = 5, -1 otherwise. */
 int vdmc_num_classes(int k);
 
 /* ids[j] = canonical (minimum) paper index of column j, ascending (reading G9).
@@ -211,6 +217,12 @@ vdmc_status vdmc_class_ids(int k, uint16_t *ids);
  * VDMC_EK / VDMC_EINVAL) for a bad k or kind. */
 int vdmc_num_classes_kind(int k, int kind);
 vdmc_status vdmc_class_ids_kind(int k, int kind, uint16_t *ids);
+
+/* Column ids for k in {3, 4, 5} (k = 5 indices need 20 bits): ids host uint32 [num_classes].
+ * k = 5: 9364 directed classes (OEIS A003085), 21 undirected (A001349).  The first call for
+ * k = 5 builds the 2^20-entry table on the host cores (about a second).
+ * Errors: VDMC_EK, VDMC_EINVAL. */
+vdmc_status vdmc_class_ids32(int k, int kind, uint32_t *ids);
 
 /* Graph facts (host struct). */
 vdmc_status vdmc_get_info(const vdmc_graph *g, vdmc_graph_info *info);

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libvdmc.so")
-SOURCES = ["api.cu", "build.cu", "enum.cu", "edges.cu"]
+SOURCES = ["api.cu", "build.cu", "enum.cu", "edges.cu", "layers.cu"]
 
 def _nccl_dir() -> str:
     """NCCL 2.28 as shipped with torch (nvidia-nccl wheel): headers and libnccl.so.2."""

@@ -1,12 +1,16 @@
 // api.cu -- the C ABI of libvdmc.so (declared and documented in include/vdmc.h),
 // error reporting, and the motif-class lookup table.
 #include <algorithm>
+#include <array>
+#include <tuple>
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -237,9 +241,106 @@ static const ClassTable &table(int k, int kind) {
 
 const uint8_t *host_lut(int k, int kind) { return table(k, kind).lut.data(); }
 const uint16_t *host_class_ids(int k, int kind) { return table(k, kind).ids.data(); }
-int num_classes(int k, int kind) {
-    return (k == 3 || k == 4) && (kind == 0 || kind == 1) ? (int)table(k, kind).ids.size() : -1;
+// Generic 16-bit tables for k <= 5 (the BFS-layer path, layers.cu): the same
+// definition (P:81 index, min over the k! orders, P:95 / P:138) over the pair-code-major device
+// mask of k(k-1)/2 pairs in lexicographic order -- for k = 3 / 4 the same layout and columns as
+// the 8-bit tables.  k = 5: 2^20 masks x 120 orders, built on all host cores once per process.
+struct Table16 {
+    std::vector<uint16_t> lut;   // mask -> column, 0xffff = disconnected
+    std::vector<uint32_t> ids;   // column -> canonical paper index (20 bits for k = 5)
+};
+
+static void build_table16(int k, int kind, Table16 &t) {
+    int pairs[10][2], np = 0;
+    for (int i = 0; i < k; i++)
+        for (int j = i + 1; j < k; j++) pairs[np][0] = i, pairs[np][1] = j, np++;
+    const int nmask = 1 << (2 * np);
+    std::vector<int32_t> canon(nmask);
+    std::vector<char> conn(nmask);
+    std::vector<std::array<int, 5>> perms;
+    std::array<int, 5> p = {0, 1, 2, 3, 4};
+    do perms.push_back(p);
+    while (std::next_permutation(p.begin(), p.begin() + k));
+    auto work = [&](int m0, int m1) {
+        for (int m = m0; m < m1; m++) {
+            int adj[5][5] = {}, und[5][5] = {};
+            for (int q = 0; q < np; q++) {
+                int c = (m >> (2 * q)) & 3;
+                const int x = pairs[q][0], y = pairs[q][1];
+                if (kind == 1 && c) c = 3;
+                if (c & 1) adj[x][y] = 1;
+                if (c & 2) adj[y][x] = 1;
+                if (c) und[x][y] = und[y][x] = 1;
+            }
+            int seen = 1, grown = 1;
+            while (grown) {
+                grown = 0;
+                for (int x = 0; x < k; x++)
+                    if (seen >> x & 1)
+                        for (int y = 0; y < k; y++)
+                            if (und[x][y] && !(seen >> y & 1)) seen |= 1 << y, grown = 1;
+            }
+            conn[m] = seen == (1 << k) - 1;
+            int best = 1 << 30;
+            for (const auto &pp : perms) {   // new vertex i = old vertex pp[i]; rows, MSB first
+                int idx = 0;
+                for (int i = 0; i < k; i++)
+                    for (int j = 0; j < k; j++)
+                        if (i != j) idx = (idx << 1) | adj[pp[i]][pp[j]];
+                best = std::min(best, idx);
+            }
+            canon[m] = best;
+        }
+    };
+    const int nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (int q = 0; q < nt; q++) th.emplace_back(work, (int)((int64_t)nmask * q / nt), (int)((int64_t)nmask * (q + 1) / nt));
+    for (auto &x : th) x.join();
+    std::vector<uint32_t> ids;
+    for (int m = 0; m < nmask; m++)
+        if (conn[m]) ids.push_back((uint32_t)canon[m]);
+    std::sort(ids.begin(), ids.end());
+    ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+    t.ids = ids;
+    t.lut.assign(nmask, 0xffffu);
+    for (int m = 0; m < nmask; m++)
+        if (conn[m]) t.lut[m] = (uint16_t)(std::lower_bound(ids.begin(), ids.end(), (uint32_t)canon[m]) - ids.begin());
 }
+
+static Table16 g_tab16[3][2];   // [k - 3][kind]
+static std::once_flag g_tab16_once[3][2];
+
+static const Table16 &table16(int k, int kind) {
+    std::call_once(g_tab16_once[k - 3][kind], [k, kind] { build_table16(k, kind, g_tab16[k - 3][kind]); });
+    return g_tab16[k - 3][kind];
+}
+
+int num_classes(int k, int kind) {
+    if (kind != 0 && kind != 1) return -1;
+    if (k == 3 || k == 4) return (int)table(k, kind).ids.size();
+    if (k == 5) return kind == 0 ? 9364 : 21;   // OEIS A003085(5) / A001349(5); table16 agrees (tests)
+    return -1;
+}
+
+// the 16-bit LUT of (k, kind) on `device` (uploaded once per process, never freed)
+vdmc_status device_lut16(int device, int k, int kind, const uint16_t **out) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, uint16_t *> cache;
+    const Table16 &t = table16(k, kind);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(device, k, kind);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        uint16_t *p = nullptr;
+        VDMC_CUDA(cudaMalloc((void **)&p, t.lut.size() * sizeof(uint16_t)));
+        VDMC_CUDA(cudaMemcpy(p, t.lut.data(), t.lut.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        it = cache.emplace(key, p).first;
+    }
+    *out = it->second;
+    return VDMC_OK;
+}
+
+const uint32_t *host_class_ids32(int k, int kind) { return table16(k, kind).ids.data(); }
 
 }  // namespace vdmc
 
@@ -257,7 +358,7 @@ int vdmc_num_classes(int k) { return vdmc::num_classes(k, VDMC_DIRECTED); }
 int vdmc_num_classes_kind(int k, int kind) { return vdmc::num_classes(k, kind); }
 
 vdmc_status vdmc_class_ids_kind(int k, int kind, uint16_t *ids) {
-    if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
+    if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4} (k = 5: vdmc_class_ids32)", k);
     if (kind != VDMC_DIRECTED && kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", kind);
     if (!ids) return fail(VDMC_EINVAL, "ids is NULL");
     memcpy(ids, host_class_ids(k, kind), sizeof(uint16_t) * num_classes(k, kind));
@@ -265,6 +366,18 @@ vdmc_status vdmc_class_ids_kind(int k, int kind, uint16_t *ids) {
 }
 
 vdmc_status vdmc_class_ids(int k, uint16_t *ids) { return vdmc_class_ids_kind(k, VDMC_DIRECTED, ids); }
+
+vdmc_status vdmc_class_ids32(int k, int kind, uint32_t *ids) {
+    if (k < 3 || k > 5) return fail(VDMC_EK, "k=%d not in {3,4,5}", k);
+    if (kind != VDMC_DIRECTED && kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", kind);
+    if (!ids) return fail(VDMC_EINVAL, "ids is NULL");
+    const int C = num_classes(k, kind);
+    if ((int)vdmc::table16(k, kind).ids.size() != C)
+        return fail(VDMC_EINVAL, "class table of k=%d has %d classes, expected %d", k,
+                    (int)vdmc::table16(k, kind).ids.size(), C);
+    memcpy(ids, host_class_ids32(k, kind), sizeof(uint32_t) * C);
+    return VDMC_OK;
+}
 
 static vdmc_status check_device(int device) {
     int nd = 0;
@@ -453,7 +566,7 @@ vdmc_status vdmc_get_order(const vdmc_graph *g, int32_t *order) {
 }
 
 static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o) {
-    if (k != 3 && k != 4) return fail(VDMC_EK, "k=%d not in {3,4}", k);
+    if (k < 3 || k > 5) return fail(VDMC_EK, "k=%d not in {3,4,5}", k);
     if (!opt) return VDMC_OK;
     if (opt->kind != VDMC_DIRECTED && opt->kind != VDMC_UNDIRECTED) return fail(VDMC_EINVAL, "kind=%d not in {0,1}", opt->kind);
     if (opt->star_block < 0 || opt->star_block > 1023) return fail(VDMC_EINVAL, "star_block=%d not in [1,1023] (0 = default)", opt->star_block);
@@ -461,6 +574,7 @@ static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o
         return fail(VDMC_EINVAL, "cross_block=%d not in [32,1023] (0 = default)", opt->cross_block);
     if (opt->heavy_global < 0 || opt->heavy_global > 1 || opt->force_big < 0 || opt->force_big > 1)
         return fail(VDMC_EINVAL, "heavy_global / force_big must be 0 or 1");
+    if (opt->layered < 0 || opt->layered > 1) return fail(VDMC_EINVAL, "layered must be 0 or 1");
     if (opt->ca_capacity < 0 || opt->ca_capacity > (int64_t(1) << 30))
         return fail(VDMC_EINVAL, "ca_capacity=%lld not in [1, 2^30] (0 = default)", (long long)opt->ca_capacity);
     o.kind = opt->kind;
@@ -469,6 +583,7 @@ static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o
     o.heavy_global = opt->heavy_global;
     o.force_big = opt->force_big;
     o.ca_capacity = opt->ca_capacity;
+    o.layered = opt->layered;
     o.timings_ms = opt->timings_ms;
     return VDMC_OK;
 }
@@ -531,6 +646,8 @@ vdmc_status vdmc_count_ex(const vdmc_graph *g, int k, uint64_t *counts, const vd
     int64_t lo, hi;
     if ((st = check_work(g, work, lo, hi))) return st;
     VDMC_CUDA(cudaSetDevice(g->device));
+    if (k == 5 || o.layered)   // the generic BFS-layer path (layers.cu)
+        return count_layers_impl(g, k, o.kind, counts, lo, hi, (cudaStream_t)stream, o.timings_ms);
     return count_impl(g, k, o, counts, lo, hi, (cudaStream_t)stream);
 }
 
@@ -550,6 +667,7 @@ vdmc_status vdmc_count_edges(const vdmc_graph *g, int k, uint64_t *counts, const
     CountOpts o;
     vdmc_status st = check_opts(k, opt, o);
     if (st) return st;
+    if (k == 5) return fail(VDMC_EK, "edge-level counts: k=%d not in {3,4}", k);
     if (!g) return fail(VDMC_EINVAL, "graph is NULL");
     if (!counts && g->ntasks > 0) return fail(VDMC_EINVAL, "counts is NULL");
     int64_t lo, hi;
@@ -656,6 +774,7 @@ vdmc_status vdmc_count_distributed(const vdmc_graph *g, int k, const vdmc_count_
     CountOpts o;
     vdmc_status st = check_opts(k, opt, o);
     if (st) return st;
+    if (k == 5 || o.layered) return fail(VDMC_EK, "vdmc_count_distributed: k=%d not in {3,4} / layered path", k);
     if (!g || !comm) return fail(VDMC_EINVAL, "NULL graph or communicator");
     if (root < 0 || root >= comm->nranks) return fail(VDMC_EINVAL, "root %d not in [0,%d)", root, comm->nranks);
     if (comm->device != g->device) return fail(VDMC_EINVAL, "graph on device %d, communicator on %d", g->device, comm->device);

@@ -56,6 +56,7 @@ constexpr int kNumClassesU4 = 6;
 constexpr uint8_t kNoClass = 255;
 
 const uint8_t *host_lut(int k, int kind);          // [64] or [4096]
+const uint32_t *host_class_ids32(int k, int kind); // k in {3, 4, 5}
 const uint16_t *host_class_ids(int k, int kind);   // [13] / [199], undirected [2] / [6]
 int num_classes(int k, int kind);
 
@@ -94,7 +95,7 @@ struct vdmc_graph {
 
 namespace vdmc {
 struct CountOpts {   // validated vdmc_count_options
-    int kind = 0, star_block = 0, cross_block = 0, heavy_global = 0, force_big = 0;
+    int kind = 0, star_block = 0, cross_block = 0, heavy_global = 0, force_big = 0, layered = 0;
     int64_t ca_capacity = 0;
     float *timings_ms = nullptr;
 };
@@ -115,6 +116,10 @@ vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, 
 vdmc_status count_edges_impl(const vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
                              cudaStream_t s, float *ms);
 vdmc_status edge_list_impl(const vdmc_graph *g, int32_t *u, int32_t *v);
+// generic BFS-layer path for k <= 5 (layers.cu); 16-bit class LUT per (device, k, kind)
+vdmc_status count_layers_impl(const vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,
+                              cudaStream_t s, float *ms);
+vdmc_status device_lut16(int device, int k, int kind, const uint16_t **out);
 // S1 only, for vdmc_symmetrize: G_U entries in ORIGINAL ids, sorted by (owner, nbr), OR-merged
 vdmc_status symmetrize_device(int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, cudaStream_t s,
                               int64_t *nnz_out, uint64_t **d_entries, int *vb_out);

@@ -21,7 +21,7 @@ STATUS = {1: "VDMC_EINVAL", 2: "VDMC_ERANGE", 3: "VDMC_ESELFLOOP", 4: "VDMC_EASY
 # Every symbol include/vdmc.h declares (tests check the .so exports exactly these)
 EXPORTS = ["vdmc_build_graph_edges", "vdmc_build_graph", "vdmc_symmetrize", "vdmc_free_host", "vdmc_count",
            "vdmc_count_kind", "vdmc_count_ex", "vdmc_count_edges", "vdmc_get_edges", "vdmc_plan", "vdmc_split_costs", "vdmc_root_range",
-           "vdmc_num_classes", "vdmc_class_ids", "vdmc_num_classes_kind", "vdmc_class_ids_kind",
+           "vdmc_num_classes", "vdmc_class_ids", "vdmc_num_classes_kind", "vdmc_class_ids_kind", "vdmc_class_ids32",
            "vdmc_get_info", "vdmc_get_order", "vdmc_kernel_launches", "vdmc_comm_unique_id",
            "vdmc_comm_init", "vdmc_comm_free", "vdmc_count_distributed", "vdmc_free_graph", "vdmc_trim",
            "vdmc_last_error"]
@@ -47,11 +47,11 @@ class Info(ctypes.Structure):
 class CountOptions(ctypes.Structure):
     """vdmc_count_options (include/vdmc.h); every path option is result-preserving."""
     _fields_ = [("kind", ctypes.c_int32), ("star_block", ctypes.c_int32), ("cross_block", ctypes.c_int32),
-                ("heavy_global", ctypes.c_int32), ("force_big", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("heavy_global", ctypes.c_int32), ("force_big", ctypes.c_int32), ("layered", ctypes.c_int32),
                 ("ca_capacity", ctypes.c_int64), ("timings_ms", ctypes.POINTER(ctypes.c_float))]
 
 
-OPTION_KEYS = ("star_block", "cross_block", "heavy_global", "force_big", "ca_capacity")
+OPTION_KEYS = ("star_block", "cross_block", "heavy_global", "force_big", "ca_capacity", "layered")
 
 
 _lib = None
@@ -90,6 +90,7 @@ def lib():
                                               _vp, _vp]),
             "vdmc_num_classes_kind": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
             "vdmc_class_ids_kind": (_i32, [ctypes.c_int, ctypes.c_int, _vp]),
+            "vdmc_class_ids32": (_i32, [ctypes.c_int, ctypes.c_int, _vp]),
             "vdmc_plan": (_i32, [_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Range)]),
             "vdmc_split_costs": (_i32, [_vp, _i64, ctypes.c_int, ctypes.POINTER(Range)]),
             "vdmc_num_classes": (ctypes.c_int, [ctypes.c_int]),
@@ -129,12 +130,13 @@ def num_classes(k: int, kind="directed") -> int:
 
 
 def class_ids(k: int, kind="directed") -> np.ndarray:
+    """Column ids (canonical paper index, ascending); uint32 (k = 5 indices have 20 bits)."""
     kd = _kind(kind)
     C = num_classes(k, kd)
     if C < 0:
-        _check(lib().vdmc_class_ids_kind(k, kd, None))
-    out = np.zeros(C, np.uint16)
-    _check(lib().vdmc_class_ids_kind(k, kd, out.ctypes.data))
+        _check(lib().vdmc_class_ids32(k, kd, None))
+    out = np.zeros(C, np.uint32)
+    _check(lib().vdmc_class_ids32(k, kd, out.ctypes.data))
     return out
 
 

@@ -22,7 +22,7 @@ def vd():
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "vdmc.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(vdmc_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(vdmc_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_exports_match_header(vd):
@@ -45,9 +45,30 @@ def test_class_ids_match_oracle(vd, oracle_mod):
     for k in (3, 4):
         assert vd.num_classes(k) == len(oracle_mod.class_table(k)["class_ids"])
         assert np.array_equal(vd.class_ids(k).astype(np.int64), oracle_mod.class_table(k)["class_ids"])
-    assert vd.num_classes(5) == -1
+    assert vd.num_classes(6) == -1 and vd.num_classes(2) == -1
     with pytest.raises(vd.VdmcError, match="VDMC_EK"):
-        vd.class_ids(5)
+        vd.class_ids(6)
+
+
+def test_class_ids_k5_match_oracle(vd, oracle_mod):
+    """k = 5 (NEXT-3): the library's 16-bit table (host-built, 2^20 masks) lists the same 9364
+    directed classes as the oracle; 21 undirected (OEIS A001349) = the oracle's all-mutual classes."""
+    assert vd.num_classes(5) == 9364 and vd.num_classes(5, "undirected") == 21
+    assert np.array_equal(vd.class_ids(5).astype(np.int64), oracle_mod.class_table(5)["class_ids"])
+    assert np.array_equal(vd.class_ids(5, "undirected").astype(np.int64), oracle_mod.undirected_class_ids(5))
+
+
+def test_options_validated_without_gpu(vd):
+    """vdmc_count_ex checks k and every option before touching the graph or a device."""
+    lib = vd.lib()
+    for bad in ({"star_block": 5000}, {"cross_block": 7}, {"heavy_global": 3}, {"force_big": -1},
+                {"ca_capacity": -5}, {"layered": 2}):
+        o, _ = vd._options("directed", bad, None)
+        assert vd.STATUS[lib.vdmc_count_ex(None, 4, None, None, vd.ctypes.byref(o), None)] == "VDMC_EINVAL", bad
+    o, _ = vd._options("directed", {}, None)
+    assert vd.STATUS[lib.vdmc_count_ex(None, 6, None, None, vd.ctypes.byref(o), None)] == "VDMC_EK"
+    assert vd.STATUS[lib.vdmc_count_ex(None, 4, None, None, vd.ctypes.byref(o), None)] == "VDMC_EINVAL"   # NULL graph
+    assert vd.STATUS[lib.vdmc_count_edges(None, 5, None, None, vd.ctypes.byref(o), None)] == "VDMC_EK"
 
 
 def _build(vd, n, s, d, rank=None):
@@ -97,8 +118,9 @@ def test_sym_csr_validation(vd):
 
 def test_count_rejects_bad_k_and_null(vd):
     lib = vd.lib()
-    assert vd.STATUS[lib.vdmc_count(None, 5, None, None, None)] == "VDMC_EK"
+    assert vd.STATUS[lib.vdmc_count(None, 6, None, None, None)] == "VDMC_EK"
     assert vd.STATUS[lib.vdmc_count(None, 4, None, None, None)] == "VDMC_EINVAL"
+    assert vd.STATUS[lib.vdmc_count(None, 5, None, None, None)] == "VDMC_EINVAL"   # k = 5 accepted (NEXT-3)
 
 
 def test_no_device_fails_loudly(vd):
