@@ -90,6 +90,9 @@ typedef struct {
  *   ca_capacity  entries of the per-CTA scratch holding the R-neighbour lists of a heavy
  *                task's depth-2 vertices (default 65536); a task whose lists do not fit
  *                enumerates its "2+1" sets one depth-2 vertex at a time instead
+ *   acc64        1 = 64-bit accumulator words even when 32 bits provably suffice (the library
+ *                uses 32-bit words when 6 maxdeg^3 < 2^32 (k = 4) / 2 maxdeg^2 < 2^32 (k = 3):
+ *                a bound on the connected sets through one vertex, so no count can wrap)
  *   layered      1 = the generic BFS-layer path (layers.cu; the only path for k = 5) for k = 3 / 4
  *   timings_ms   NULL, or host float[4] filled with device times (schedule + memset, enumerate,
  *                finalise, whole call); the call then synchronises `stream` before returning */
@@ -100,6 +103,8 @@ typedef struct {
     int32_t heavy_global;
     int32_t force_big;
     int32_t layered;
+    int32_t acc64;
+    int32_t reserved0;
     int64_t ca_capacity;
     float *timings_ms;
 } vdmc_count_options;

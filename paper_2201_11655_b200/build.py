@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libvdmc.so")
-SOURCES = ["api.cu", "build.cu", "enum.cu", "edges.cu", "layers.cu"]
+SOURCES = ["api.cu", "build.cu", "enum.cu", "enum32.cu", "edges.cu", "layers.cu"]
 
 def _nccl_dir() -> str:
     """NCCL 2.28 as shipped with torch (nvidia-nccl wheel): headers and libnccl.so.2."""
@@ -30,7 +30,7 @@ def build(force: bool = False, verbose: bool = False, lib: str = LIB, defines=()
     """Compile and link libvdmc.so.  defines=("VDMC_PROFILING",) gives the profiling variant
     (tools/ only: switches that drop work for phase timings)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "vdmc_internal.cuh"),
+    deps = srcs + [os.path.join(CSRC, "vdmc_internal.cuh"), os.path.join(CSRC, "enum.cu"),
                    os.path.join(HERE, "..", "include", "vdmc.h")]
     if not force and os.path.exists(lib) and \
             os.path.getmtime(lib) >= max(os.path.getmtime(d) for d in deps):

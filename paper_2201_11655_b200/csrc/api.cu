@@ -575,6 +575,7 @@ static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o
     if (opt->heavy_global < 0 || opt->heavy_global > 1 || opt->force_big < 0 || opt->force_big > 1)
         return fail(VDMC_EINVAL, "heavy_global / force_big must be 0 or 1");
     if (opt->layered < 0 || opt->layered > 1) return fail(VDMC_EINVAL, "layered must be 0 or 1");
+    if (opt->acc64 < 0 || opt->acc64 > 1) return fail(VDMC_EINVAL, "acc64 must be 0 or 1");
     if (opt->ca_capacity < 0 || opt->ca_capacity > (int64_t(1) << 30))
         return fail(VDMC_EINVAL, "ca_capacity=%lld not in [1, 2^30] (0 = default)", (long long)opt->ca_capacity);
     o.kind = opt->kind;
@@ -584,6 +585,7 @@ static vdmc_status check_opts(int k, const vdmc_count_options *opt, CountOpts &o
     o.force_big = opt->force_big;
     o.ca_capacity = opt->ca_capacity;
     o.layered = opt->layered;
+    o.acc64 = opt->acc64;
     o.timings_ms = opt->timings_ms;
     return VDMC_OK;
 }
@@ -611,12 +613,15 @@ static vdmc_status count_impl(const vdmc_graph *g, int k, const CountOpts &o, ui
         for (auto &e : ev) VDMC_CUDA(cudaEventCreate(&e));
         VDMC_CUDA(cudaEventRecord(ev[0], s));
     }
-    unsigned long long *acc = nullptr;
-    VDMC_CUDA(dalloc((void **)&acc, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
-    vdmc_status st = count_into(g, k, o, acc, lo, hi, s, o.timings_ms ? ms3 : nullptr);
+    const bool a32 = !o.acc64 && counts_fit_u32(g, k);   // 32-bit words when no count can exceed 2^32
+    void *acc = nullptr;
+    VDMC_CUDA(dalloc(&acc, (size_t)std::max<int64_t>(g->n, 1) * C * (a32 ? 4 : 8), s));
+    vdmc_status st = a32 ? count_into32(g, k, o, (unsigned int *)acc, lo, hi, s, o.timings_ms ? ms3 : nullptr)
+                         : count_into(g, k, o, (unsigned long long *)acc, lo, hi, s, o.timings_ms ? ms3 : nullptr);
     if (st == VDMC_OK) {
         if (o.timings_ms) cudaEventRecord(ev[1], s);
-        st = finalize(g, C, acc, counts, s);
+        st = a32 ? finalize32(g, C, (const unsigned int *)acc, counts, s)
+                 : finalize(g, C, (const unsigned long long *)acc, counts, s);
         if (o.timings_ms) cudaEventRecord(ev[2], s);
     }
     dfree(acc, s);
@@ -786,16 +791,20 @@ vdmc_status vdmc_count_distributed(const vdmc_graph *g, int k, const vdmc_count_
     const vdmc_range my = parts[(size_t)comm->rank];
     const int C = num_classes(k, o.kind);
     const size_t elems = (size_t)std::max<int64_t>(g->n, 1) * C;
-    unsigned long long *acc = nullptr;
-    VDMC_CUDA(dalloc((void **)&acc, elems * sizeof(uint64_t), s));
+    const bool a32 = !o.acc64 && counts_fit_u32(g, k);   // the full sums fit 32 bits, so do the partials
+    void *acc = nullptr;
+    VDMC_CUDA(dalloc(&acc, elems * (a32 ? 4 : 8), s));
     o.timings_ms = nullptr;
-    st = count_into(g, k, o, acc, my.task_lo, my.task_hi, s, nullptr);
+    st = a32 ? count_into32(g, k, o, (unsigned int *)acc, my.task_lo, my.task_hi, s, nullptr)
+             : count_into(g, k, o, (unsigned long long *)acc, my.task_lo, my.task_hi, s, nullptr);
     if (st == VDMC_OK) {
-        // sum of the class-major partials (uint64 wrap-around addition: exact), then the root
+        // sum of the class-major partials (unsigned wrap-around addition: exact), then the root
         // restores rows in place of original ids
-        ncclResult_t r = ncclReduce(acc, acc, elems, ncclUint64, ncclSum, root, comm->comm, s);
+        ncclResult_t r = ncclReduce(acc, acc, elems, a32 ? ncclUint32 : ncclUint64, ncclSum, root, comm->comm, s);
         if (r != ncclSuccess) st = fail(VDMC_ENCCL, "ncclReduce: %s", ncclGetErrorString(r));
-        else if (comm->rank == root) st = finalize(g, C, acc, counts, s);
+        else if (comm->rank == root)
+            st = a32 ? finalize32(g, C, (const unsigned int *)acc, counts, s)
+                     : finalize(g, C, (const unsigned long long *)acc, counts, s);
     }
     dfree(acc, s);
     return st;

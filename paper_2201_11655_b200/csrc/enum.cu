@@ -39,8 +39,22 @@
 
 #include "vdmc_internal.cuh"
 
+// The accumulator word: u64, or u32 when every count provably fits (enum32.cu compiles this file
+// again with VDMC_ACC32 = 1; the host picks it when 6 * maxdeg^3 < 2^32, a bound on the connected
+// 4-sets through one vertex, so no (vertex, class) count can wrap).  Halving the n x C matrix
+// keeps twice as many of its hot class columns in L2.
+#ifndef VDMC_ACC32
+#define VDMC_ACC32 0
+#endif
+
 namespace vdmc {
 namespace {
+
+#if VDMC_ACC32
+using AccT = unsigned int;
+#else
+using AccT = unsigned long long;
+#endif
 
 constexpr int kWarps = 16;            // warps per CTA
 constexpr int kBlock = kWarps * 32;
@@ -66,7 +80,7 @@ struct Dev {
     const int32_t *__restrict__ heavy_task;   // task ids of heavy roots, rank order
     const int32_t *__restrict__ light_root;   // light roots, rank order
     int64_t nheavy, nlight;
-    unsigned long long *__restrict__ acc;     // accumulator, class-major: element (v = rank, col) at col * ns + v
+    AccT *__restrict__ acc;                   // accumulator, class-major: element (v = rank, col) at col * ns + v
     uint32_t ns;                              // column stride = n
     uint32_t *__restrict__ gheavy;            // global fallback: per-CTA heavy buffers
     uint32_t *__restrict__ glight;            // global fallback: per-warp oversize L_a + bitmap
@@ -111,7 +125,7 @@ constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool + 2 
 // sets share sectors with other vertices' updates of the same (hot) class, so a matrix far
 // larger than L2 still hits L2 for the few classes that dominate (cfg5: 417 -> 352 ms vs
 // row-major, profiles/r01_v8_*); rows are restored by k_finalize.
-__device__ __forceinline__ unsigned long long *accp(const Dev &g, uint32_t v, uint32_t col) {
+__device__ __forceinline__ AccT *accp(const Dev &g, uint32_t v, uint32_t col) {
     return g.acc + ((size_t)col * g.ns + v);
 }
 
@@ -145,13 +159,24 @@ __device__ __forceinline__ uint32_t swap2(uint32_t c) { return ((c & 1u) << 1) |
 __device__ __forceinline__ uint32_t get2(const uint32_t *B, int p) { return (B[p >> 4] >> ((p & 15) << 1)) & 3u; }
 __device__ __forceinline__ void set2(uint32_t *B, int p, uint32_t code) { atomicOr(B + (p >> 4), code << ((p & 15) << 1)); }
 
-// predicated fire-and-forget u64 add (no divergent branch around it in the uniform b loops)
+// predicated fire-and-forget add (no divergent branch around it in the uniform b loops)
+#if !VDMC_ACC32
 __device__ __forceinline__ void red_if(bool p, unsigned long long *addr, uint32_t v) {
     asm volatile(
         "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u64 [%0], %1;\n\t}\n" ::"l"(addr),
         "l"((unsigned long long)v), "r"((uint32_t)p)
         : "memory");
 }
+__device__ __forceinline__ void acc_add(unsigned long long *p, uint32_t v) { atomicAdd(p, (unsigned long long)v); }
+#else
+__device__ __forceinline__ void red_if(bool p, unsigned int *addr, uint32_t v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.global.add.u32 [%0], %1;\n\t}\n" ::"l"(addr),
+        "r"(v), "r"((uint32_t)p)
+        : "memory");
+}
+__device__ __forceinline__ void acc_add(unsigned int *p, uint32_t v) { atomicAdd(p, v); }
+#endif
 
 // predicated shared-memory u32 reduction (histograms)
 __device__ __forceinline__ void red_shared_if(bool p, uint32_t *addr, uint32_t v) {
@@ -192,8 +217,8 @@ __device__ __forceinline__ void flush_hist(uint32_t *H, const Dev &g, uint32_t r
     for (int j = lane; j < C; j += 32) {
         const uint32_t v = H[j];
         if (v) {
-            atomicAdd(accp(g, r, j), (unsigned long long)v);
-            atomicAdd(accp(g, a, j), (unsigned long long)v);
+            acc_add(accp(g, r, j), v);
+            acc_add(accp(g, a, j), v);
             H[j] = 0;
         }
     }
@@ -386,7 +411,7 @@ constexpr uint32_t kInfPos = 0x3fffffffu;
 
 // row offset of vertex v's column col in the accumulator (32-bit when n*C < 2^32)
 template <int C, bool OFF32>
-__device__ __forceinline__ unsigned long long *acc_at(const Dev &g, uint32_t v, uint32_t col) {
+__device__ __forceinline__ AccT *acc_at(const Dev &g, uint32_t v, uint32_t col) {
     if (OFF32) return g.acc + (col * g.ns + v);
     return g.acc + ((size_t)col * g.ns + v);
 }
@@ -425,7 +450,7 @@ __device__ __forceinline__ void star_flush_c(const Dev &g, const uint8_t *lut, u
     for (uint32_t crb = 1; crb <= 3; crb++) {
         if (n[crb - 1]) {
             const int col = lut[lmask | crb << 2];
-            atomicAdd(accp(g, c, col), (unsigned long long)n[crb - 1]);
+            acc_add(accp(g, c, col), n[crb - 1]);
             atomicAdd(H + col, n[crb - 1]);
         }
     }
@@ -467,12 +492,12 @@ __device__ __forceinline__ void star_event(const Dev &g, const uint8_t *lut, uin
             const uint32_t cbc = hit ? swap2(g.nr_adj[s.q[t]] & 3u) : 0u;   // the entry holds code(c, b)
             const uint32_t lmask = cra | ((key % 3u) + 1u) << 4 | (key / 3u) << 8;
             col = lut[lmask | crb << 2 | cab << 6 | cbc << 10];
-            atomicAdd(accp(g, R[p] >> 2, col), 1ull);
+            acc_add(accp(g, R[p] >> 2, col), 1u);
             atomicAdd(H + col, 1u);
             if (!aev) s.d[t] -= inc_of(crb);   // U will count this j for every c: take it back for this one
         }
         const unsigned m = __match_any_sync(kFull, col);
-        if (col != kNone && lane == __ffs(m) - 1) atomicAdd(accp(g, b, col), (unsigned long long)__popc(m));
+        if (col != kNone && lane == __ffs(m) - 1) acc_add(accp(g, b, col), __popc(m));
         if (!aev) {
             for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
                 const uint32_t kk = __shfl_sync(kFull, key, __ffs(hm) - 1);
@@ -484,7 +509,7 @@ __device__ __forceinline__ void star_event(const Dev &g, const uint8_t *lut, uin
     if (!aev) {
         s.U += inc_of(crb);
         const unsigned cnt = s.cntk - nh;
-        if (cnt) atomicAdd(accp(g, b, ((s.cols >> (crb << 3)) & 0xffu)), (unsigned long long)cnt);
+        if (cnt) acc_add(accp(g, b, ((s.cols >> (crb << 3)) & 0xffu)), cnt);
     }
 }
 
@@ -787,7 +812,7 @@ __device__ __forceinline__ void cross_flush(const Dev &g, const uint8_t *lut, ui
             for (uint32_t crj = 1; crj <= 3; crj++) {
                 if (n[crj - 1]) {
                     const int col = PART == 1 ? lut[cra | crj << 2 | cxc << 8] : lut[crj | cra << 2 | cxc << 10];
-                    atomicAdd(accp(g, c, col), (unsigned long long)n[crj - 1]);
+                    acc_add(accp(g, c, col), n[crj - 1]);
                     atomicAdd(H + col, n[crj - 1]);
                 }
             }
@@ -848,12 +873,12 @@ __device__ __forceinline__ void cross_part(const Dev &g, const uint8_t *lut, uin
                 } else {
                     col = lut[crj | cra << 2 | swap2(cxj) << 6 | cxc << 10];
                 }
-                atomicAdd(accp(g, c, col), 1ull);
+                acc_add(accp(g, c, col), 1u);
                 atomicAdd(H + col, 1u);
             }
             if (hit && !aev) s.d[t] -= inc_of(crj);   // U will count this j for every c: take it back
             const unsigned m = __match_any_sync(kFull, col);
-            if (col != kNone && lane == __ffs(m) - 1) atomicAdd(accp(g, b, col), (unsigned long long)__popc(m));
+            if (col != kNone && lane == __ffs(m) - 1) acc_add(accp(g, b, col), __popc(m));
             if (!aev) {
                 const uint32_t key = valid ? (La[q] & 3u) - 1u : 15u;
                 for (unsigned hm = __ballot_sync(kFull, hit); hm; hm &= hm - 1) {
@@ -866,7 +891,7 @@ __device__ __forceinline__ void cross_part(const Dev &g, const uint8_t *lut, uin
         if (!aev) {
             s.U += inc_of(crj);
             const unsigned cnt = s.cntk - nh;
-            if (cnt) atomicAdd(accp(g, b, ((s.cols >> (crj << 3)) & 0xffu)), (unsigned long long)cnt);
+            if (cnt) acc_add(accp(g, b, ((s.cols >> (crj << 3)) & 0xffu)), cnt);
         }
         j++;
         if (anext < j) anext = next_a_event(codes, j, j1, lane);
@@ -1261,7 +1286,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
 constexpr int kFinV = 16;
 template <int C>
 __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int32_t *__restrict__ order,
-                                                  const unsigned long long *__restrict__ acc,
+                                                  const AccT *__restrict__ acc,
                                                   unsigned long long *__restrict__ out) {
     __shared__ unsigned long long tile[kFinV][C + 1];
     for (int64_t v0 = (int64_t)blockIdx.x * kFinV; v0 < n; v0 += (int64_t)gridDim.x * kFinV) {
@@ -1454,6 +1479,7 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
 
 }  // namespace
 
+#if !VDMC_ACC32   // graph-level host code: compiled once (enum.cu), not in enum32.cu
 // S3 (device copies of the class LUTs) + S4 schedule, built once per graph at the end of a build:
 // heavy / light work lists and the induced adjacency of every heavy root's N+(r).
 vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s) {
@@ -1590,6 +1616,8 @@ vdmc_status plan_prefix(const vdmc_graph *g, int k, int64_t *prefix_host, cudaSt
     return VDMC_OK;
 }
 
+#endif  // !VDMC_ACC32
+
 namespace {
 struct Events {   // per-call timing events (only when the caller asks for timings)
     cudaEvent_t e[4] = {};
@@ -1601,7 +1629,7 @@ struct Events {   // per-call timing events (only when the caller asks for timin
 }  // namespace
 
 template <int K, int C>
-static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts &o, unsigned long long *acc,
+static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts &o, AccT *acc,
                        int64_t lo, int64_t hi, cudaStream_t s, float *ms3) {
     const int dev = g->device;
     int nsm = 0;
@@ -1631,7 +1659,7 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     unsigned long long *ctr = nullptr;
     VDMC_CUDA(dalloc((void **)&scratch, need * sizeof(uint32_t), s));
     VDMC_CUDA(dalloc((void **)&ctr, 2 * sizeof(unsigned long long), s));
-    VDMC_CUDA(cudaMemsetAsync(acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(uint64_t), s));
+    VDMC_CUDA(cudaMemsetAsync(acc, 0, (size_t)std::max<int64_t>(g->n, 1) * C * sizeof(AccT), s));
     VDMC_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
     if (ms3) VDMC_CUDA(cudaEventRecord(ev.e[1], s));
     trace("scratch+memset");
@@ -1688,8 +1716,16 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     return VDMC_OK;
 }
 
-vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned long long *acc, int64_t lo,
-                       int64_t hi, cudaStream_t s, float *ms3) {
+#if VDMC_ACC32
+#define VDMC_COUNT_INTO count_into32
+#define VDMC_FINALIZE finalize32
+#else
+#define VDMC_COUNT_INTO count_into
+#define VDMC_FINALIZE finalize
+#endif
+
+vdmc_status VDMC_COUNT_INTO(const vdmc_graph *g, int k, const CountOpts &o, AccT *acc, int64_t lo, int64_t hi,
+                            cudaStream_t s, float *ms3) {
     const uint8_t *lut = g->lut[o.kind][k == 4 ? 1 : 0];
     if (o.kind == VDMC_UNDIRECTED)
         return k == 3 ? run<3, kNumClassesU3>(g, lut, o, acc, lo, hi, s, ms3)
@@ -1699,13 +1735,13 @@ vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned 
 }
 
 template <int C>
-static void launch_finalize(int64_t n, const int32_t *order, const unsigned long long *acc, uint64_t *counts, int nsm,
+static void launch_finalize(int64_t n, const int32_t *order, const AccT *acc, uint64_t *counts, int nsm,
                             cudaStream_t s) {
     const unsigned fg = (unsigned)std::min<int64_t>((n + kFinV - 1) / kFinV, (int64_t)nsm * 8);
     k_finalize<C><<<fg, 256, 0, s>>>(n, order, acc, (unsigned long long *)counts);
 }
 
-vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, uint64_t *counts, cudaStream_t s) {
+vdmc_status VDMC_FINALIZE(const vdmc_graph *g, int C, const AccT *acc, uint64_t *counts, cudaStream_t s) {
     if (g->n <= 0) return VDMC_OK;
     int nsm = 0;
     VDMC_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));

@@ -96,6 +96,7 @@ struct vdmc_graph {
 namespace vdmc {
 struct CountOpts {   // validated vdmc_count_options
     int kind = 0, star_block = 0, cross_block = 0, heavy_global = 0, force_big = 0, layered = 0;
+    int acc64 = 0;   // 1 = force the 64-bit accumulator even when 32 bits provably suffice
     int64_t ca_capacity = 0;
     float *timings_ms = nullptr;
 };
@@ -111,6 +112,15 @@ vdmc_status count_into(const vdmc_graph *g, int k, const CountOpts &o, unsigned 
                        int64_t hi, cudaStream_t s, float *ms3);
 // class-major rank-order accumulator -> row-major [original id][C]
 vdmc_status finalize(const vdmc_graph *g, int C, const unsigned long long *acc, uint64_t *counts, cudaStream_t s);
+// the same with a 32-bit accumulator (enum32.cu), used when every count provably fits 32 bits
+vdmc_status count_into32(const vdmc_graph *g, int k, const CountOpts &o, unsigned int *acc, int64_t lo, int64_t hi,
+                         cudaStream_t s, float *ms3);
+vdmc_status finalize32(const vdmc_graph *g, int C, const unsigned int *acc, uint64_t *counts, cudaStream_t s);
+// true if every (vertex, class) count of a k-count fits 32 bits (bound on sets through a vertex)
+inline bool counts_fit_u32(const vdmc_graph *g, int k) {
+    const double d = (double)g->max_degree;
+    return (k == 3 ? 2.0 * d * d : 6.0 * d * d * d) < 4294967296.0;
+}
 // edge-level counts (edges.cu): counts [edges][C] in the canonical edge order; ms (optional,
 // host float[4]) as vdmc_count_options.timings_ms
 vdmc_status count_edges_impl(const vdmc_graph *g, int k, int kind, uint64_t *counts, int64_t lo, int64_t hi,

@@ -48,10 +48,11 @@ class CountOptions(ctypes.Structure):
     """vdmc_count_options (include/vdmc.h); every path option is result-preserving."""
     _fields_ = [("kind", ctypes.c_int32), ("star_block", ctypes.c_int32), ("cross_block", ctypes.c_int32),
                 ("heavy_global", ctypes.c_int32), ("force_big", ctypes.c_int32), ("layered", ctypes.c_int32),
+                ("acc64", ctypes.c_int32), ("reserved0", ctypes.c_int32),
                 ("ca_capacity", ctypes.c_int64), ("timings_ms", ctypes.POINTER(ctypes.c_float))]
 
 
-OPTION_KEYS = ("star_block", "cross_block", "heavy_global", "force_big", "ca_capacity", "layered")
+OPTION_KEYS = ("star_block", "cross_block", "heavy_global", "force_big", "ca_capacity", "layered", "acc64")
 
 
 _lib = None

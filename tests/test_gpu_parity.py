@@ -304,3 +304,15 @@ def test_64bit_accumulator_offsets(vd, oracle_mod):
         del out
     gr.close()
     vd.trim(torch.cuda.current_device())
+
+
+@pytest.mark.parametrize("name,scale", [("cfg3", 0.03), ("cfg5", 0.002), ("cfg2", 1.0)])
+def test_acc32_equals_acc64(vd, oracle_mod, name, scale):
+    """Graphs whose largest degree makes every count provably < 2^32 (6 maxdeg^3 < 2^32) run with a
+    32-bit accumulator by default; forcing 64-bit words gives the same matrix, and both the oracle's."""
+    g = G.make_config(name, scale=scale)
+    deg = np.bincount(np.concatenate([g[1], g[2]]), minlength=g[0])
+    assert 6 * float(deg.max()) ** 3 < 2 ** 32
+    want = oracle_mod.count_esu(g, 4)
+    assert np.array_equal(gpu_count(vd, g, 4), want)
+    assert np.array_equal(gpu_count(vd, g, 4, options={"acc64": 1}), want)
