@@ -125,3 +125,21 @@ def test_eq4_undirected_gnp(oracle_mod, k):
     assert (np.abs(m[ok] - 1.0) <= 4 * se[ok] + 0.01).all(), (m, se, E)
     mid = (E >= 10) & ~ok                 # Poisson-like: 6 SE + 3 sqrt(E / R) / E
     assert (np.abs(m[mid] - 1.0) <= 6 * se[mid] + 3 / np.sqrt(E[mid] * R)).all(), (m, se, E)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_count_vertex_undirected_vs_pure_python(oracle_mod, k):
+    """count_vertex_undirected (per-vertex ESU on G_U) pinned to the table-free pure-Python brute
+    force on random graphs, and on a star centre to the closed form C(L, k-1)."""
+    ids = oracle_mod.undirected_class_ids(k).tolist()
+    for seed in range(12):
+        n = 6 + seed % 6
+        g = G.random_small(n, (0.2, 0.4, 0.6)[seed % 3], 7300 + seed)
+        want = _named(oracle_mod, g, k)
+        verts = np.array(sorted({0, n // 2, n - 1}), np.int32)
+        assert np.array_equal(oracle_mod.count_vertex_undirected(g, k, verts), want[verts]), seed
+    L = 11
+    row = oracle_mod.count_vertex_undirected(G.out_star(L), k, np.array([0, 3], np.int32))
+    col = ids.index(GOLD["uclass"][k]["path" if k == 3 else "star"])
+    assert row[0, col] == math.comb(L, k - 1) and row[0].sum() == math.comb(L, k - 1)
+    assert row[1, col] == math.comb(L - 1, k - 2) and row[1].sum() == math.comb(L - 1, k - 2)
