@@ -81,7 +81,9 @@ typedef struct {
  * means "the default".  All path options are RESULT-PRESERVING: they choose how the same sets
  * are enumerated, never which (tests force each path and compare with the oracle).
  *   kind         VDMC_DIRECTED (0) or VDMC_UNDIRECTED
- *   star_block   b positions per heavy "3" work item, in [1, 1023] (default 1023)
+ *   star_block   0 (default): the heavy "3" sets are counted in closed form per task (key
+ *                histograms of N+(r) plus the sets with an induced edge, classified one by one);
+ *                in [1, 1023]: they are enumerated instead, in work items of that many b positions
  *   cross_block  R positions per heavy "2+1" work item, in [32, 1023] (default 256)
  *   heavy_global 1 = heavy-task buffers in global memory (the path taken when the largest
  *                degree does not fit shared memory)

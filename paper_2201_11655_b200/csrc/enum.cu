@@ -558,6 +558,93 @@ __device__ __forceinline__ void star_fast_any(const Dev &g, const uint32_t *R, S
     }
 }
 
+// ---------------------------------------------- shape "3" at heavy roots, counted in closed form
+// Task (r, a = R[i]), Y = code(r, a): the star sets {r, a, R[j], R[p]}, i < j < p.  The key of a
+// position q > i is codes[q] = x_q | al_q << 2 with x_q = code(r, R[q]) and al_q = code(a, R[q]).
+// A pair (j, p) with no R[j]-R[p] edge has the mask Y | x_j << 2 | x_p << 4 | al_j << 6 |
+// al_p << 8: its class cls(k_j, k_p) depends on the two keys only and is symmetric in them
+// (exchanging the roles of b and c relabels the same digraph; the LUT gives the minimum isomorph).
+// With N[k] = #{q > i : key k} (counted when codes[] is built):
+//   * R[q] lies in N[k'] - [k_q = k'] - #{induced neighbours of R[q] beyond i with key k'} such
+//     sets of class cls(k_q, k') for every key k' -- one atomic per key present;
+//   * r and a lie in N[k] N[k'] (k < k') or C(N[k], 2) (k = k') sets of class cls(k, k'), minus
+//     the pairs with an R[j]-R[p] edge (E[k][k'], counted below) -- added once per task;
+//   * a pair with an R[j]-R[p] edge (an event: an entry of the root's induced adjacency, k_nr) is
+//     classified alone by its full mask, code(R[j], R[p]) in bits 10-11.
+// The induced graph of N+(r) is sparse (cfg4: 51K edges over all 6585 heavy roots), so a task
+// costs O(D - i) plus its events instead of O((D - i)^2) set visits; every set is still counted
+// once, in the class of its exact mask.
+constexpr int kSPM = 2;                 // positions per lane in one closed-form star item
+constexpr int kSPW = 32 * kSPM;
+
+__device__ __forceinline__ void acc_addw(AccT *p, AccT v) { atomicAdd(p, v); }   // modular (v may be "-1")
+
+template <int C>
+__device__ __forceinline__ void star_closed_item(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, int i,
+                                                 const uint32_t *R, int D, const uint8_t *codes, const int *sN,
+                                                 int *sE, uint32_t P, int64_t seg, int q0, int lane) {
+#pragma unroll 1
+    for (int t = 0; t < kSPM; t++) {
+        const int q = q0 + 32 * t + lane;
+        if (q >= D) break;   // no warp-collective operations below
+        const uint32_t v = R[q] >> 2, kq = codes[q];
+        const uint32_t mq = cra | (kq & 3u) << 2 | (kq >> 2) << 6;   // R[q] in the b slots
+        uint64_t corr = 0;   // induced neighbours beyond i with keys 1..3 (al = 0), 21-bit fields
+        int64_t e = g.nr_off[seg + q];
+        const int64_t e1 = g.nr_off[seg + q + 1];
+        if (e1 - e > 16) {   // first entry with position > i (the list ascends in position)
+            int64_t lo = e, hi = e1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int)(g.nr_adj[mid] >> 2) <= i) lo = mid + 1;
+                else hi = mid;
+            }
+            e = lo;
+        }
+        for (; e < e1; e++) {
+            const uint32_t en = g.nr_adj[e];
+            const int p = (int)(en >> 2);
+            if (p <= i) continue;
+            const uint32_t kp = codes[p];
+            const uint32_t mp = mq | (kp & 3u) << 4 | (kp >> 2) << 8;
+            if (kp < 4u) corr += 1ull << (21u * (kp - 1u));
+            else acc_addw(accp(g, v, lut[mp]), (AccT)0 - (AccT)1);   // not plain: take it back from below
+            if (p > q) {   // the event set {r, a, R[q], R[p]}, R[q] in the b slots
+                const uint32_t col = lut[mp | (en & 3u) << 10];
+                acc_add(accp(g, v, col), 1u);
+                acc_add(accp(g, R[p] >> 2, col), 1u);
+                atomicAdd(H + col, 1u);
+                atomicAdd(sE + (min(kq, kp) << 4 | max(kq, kp)), 1);
+            }
+        }
+        for (uint32_t m = P; m; m &= m - 1u) {   // plain sets of R[q], per partner key
+            const uint32_t k = (uint32_t)__ffs(m) - 1u;
+            uint32_t cnt = (uint32_t)sN[k] - (k == kq ? 1u : 0u);
+            if (k < 4u) cnt -= (uint32_t)(corr >> (21u * (k - 1u))) & 0x1fffffu;
+            if (cnt) acc_add(accp(g, v, lut[mq | (k & 3u) << 4 | (k >> 2) << 8]), cnt);
+        }
+    }
+}
+
+// r and a: the plain pairs of every key pair, once per task (thread tid < 256: keys tid >> 4 <= tid & 15)
+template <int C>
+__device__ __forceinline__ void star_closed_root(const Dev &g, const uint8_t *lut, uint32_t r, uint32_t a,
+                                                 uint32_t cra, int *sN, int *sE, int tid) {
+    if (tid >= 256) return;
+    const uint32_t k1 = (uint32_t)tid >> 4, k2 = (uint32_t)tid & 15u;
+    const int e = sE[tid];
+    if (k1 <= k2 && (k1 & 3u) && (k2 & 3u)) {
+        const uint64_t n1 = (uint64_t)sN[k1], n2 = (uint64_t)sN[k2];
+        const uint64_t pairs = (k1 < k2 ? n1 * n2 : n1 * (n1 - (n1 > 0)) / 2) - (uint64_t)e;
+        if (pairs) {
+            const uint32_t col = lut[cra | (k1 & 3u) << 2 | (k2 & 3u) << 4 | (k1 >> 2) << 6 | (k2 >> 2) << 8];
+            acc_addw(accp(g, r, col), (AccT)pairs);
+            acc_addw(accp(g, a, col), (AccT)pairs);
+        }
+    }
+    if (e) sE[tid] = 0;
+}
+
 // first j' in [j, jend) with an a-b edge (codes[j'] >= 4), else jend
 __device__ __forceinline__ int next_a_event(const uint8_t *codes, int j, int jend, int lane) {
     for (int base = j; base < jend; base += 32) {
@@ -1050,7 +1137,8 @@ template <int K, int C, int NW>
 __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uint32_t r, int i, const uint32_t *R,
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
-                                           int *s_ca, const Staged *st, int w, int lane) {
+                                           int *s_ca, const Staged *st, int w, int lane, const int *sN = nullptr,
+                                           int *sE = nullptr) {
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -1088,13 +1176,16 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
     } else {
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(VDMC_SKIPF(g) & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
+        // shape "3": closed form (default), or the enumerated star items when the star_block option
+        // is given (chunk x block of b positions; kept as the per-set reference path)
+        const bool closed = g.fold <= 0;
+        const int fold = closed ? kMaxBlock : g.fold;
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
-        // b-block length of the star items (option; default kMaxBlock)
-        // (measured: a per-task block of ~2 items per warp, min 64, is slower on cfg4, 470 vs 456 ms,
-        // gpurun_out/r02b/ab_fold_cfg4.txt: the per-item setup outweighs the tail it removes)
-        const int fold = g.fold > 0 ? g.fold : kMaxBlock;
-        int nstar = 0;   // star items: chunk x block of b positions
-        for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
+        int nstar = 0;
+        if (closed) nstar = D - (i + 2) > 0 ? (D - (i + 1) + kSPW - 1) / kSPW : 0;
+        else
+            for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
+        const uint32_t P = __ballot_sync(kFull, closed && lane < 16 && sN[lane] > 0);   // keys present beyond i
         const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
         const int nB = cross ? nck * njb : nL;                                  // "2+1" items
         const int total = nstar + nB + nL;
@@ -1105,6 +1196,13 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
             int star_k = -1, star_b = 0, b_it = -1;
+            if (it < nstar && closed) {
+                if (!(VDMC_SKIPF(g) & 1))
+                    star_closed_item<C>(g, lut, H, cra, i, R, D, codes, sN, sE, P, g.hbase[r], i + 1 + it * kSPW, lane);
+                if (g.big) flush_hist<C>(H, g, r, a, lane);
+                __syncwarp();
+                continue;
+            }
             if (it < nstar) {
                 int rem = it, kk = 0;
                 for (;; kk++) {
@@ -1143,8 +1241,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item, s_sub[4];   // s_sub: the slice's heavy_task [h0, h1) and light_root [l0, l1)
     __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
+    __shared__ int s_N[16], s_E[256];       // closed-form star: keys beyond i, event pairs per key pair
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
+    if (tid < 256) s_E[tid] = 0;
+    if (tid < 16) s_N[tid] = 0;
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
     uint32_t *H = sm + L.hist + wid * C;
     if (tid < 4) {   // both lists ascend with the task id, so the slice [lo, hi) is a sub-list of each
@@ -1205,15 +1306,27 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 s_ca[0] = 0;
                 s_ca[1] = 0;
             }
-            if (K == 4)   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2
-                for (int q = tid; q < D; q += kBlock) codes[q] = (uint8_t)((R[q] & 3u) | get2(Ba, q) << 2);
+            if (K == 4)   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2; s_N = key counts beyond i
+                for (int base = wid * 32; base < D; base += kBlock) {
+                    const int q = base + lane;
+                    uint32_t key = 0;
+                    if (q < D) {
+                        key = (R[q] & 3u) | get2(Ba, q) << 2;
+                        codes[q] = (uint8_t)key;
+                    }
+                    const bool cnt = q > i && q < D;
+                    const unsigned m = __match_any_sync(kFull, cnt ? key : 0u);
+                    if (cnt && lane == __ffs(m) - 1) atomicAdd(s_N + key, __popc(m));
+                }
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_E);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
+            if (K == 4 && g.fold <= 0) star_closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_E, tid);
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
             __syncthreads();
+            if (tid < 16) s_N[tid] = 0;
         }
     }
     __syncthreads();
