@@ -420,7 +420,7 @@ __device__ __forceinline__ AccT *acc_at(const Dev &g, uint32_t v, uint32_t col) 
 // one set in the 10-bit field of code(r, b) in {1, 2, 3}; a block spans <= 1023 b's, so no field
 // overflows, and packed corrections (U + d) are exact field by field (final fields in [0, 1023])
 __device__ __forceinline__ uint32_t inc_of(uint32_t crb) { return 1u << (crb * 10u - 10u); }
-constexpr int kMaxBlock = 1023;
+constexpr int kMaxBlock = 1023;   // (enumerated path: star_block <= kMaxBlock, checked by the API)
 
 // c at position p: next entry of its induced list after index q with position < p, else INF
 __device__ __forceinline__ void nr_next(const Dev &g, int64_t seg, int p, uint32_t &q, uint32_t &npos) {
@@ -558,37 +558,63 @@ __device__ __forceinline__ void star_fast_any(const Dev &g, const uint32_t *R, S
     }
 }
 
-// ---------------------------------------------- shape "3" at heavy roots, counted in closed form
-// Task (r, a = R[i]), Y = code(r, a): the star sets {r, a, R[j], R[p]}, i < j < p.  The key of a
-// position q > i is codes[q] = x_q | al_q << 2 with x_q = code(r, R[q]) and al_q = code(a, R[q]).
-// A pair (j, p) with no R[j]-R[p] edge has the mask Y | x_j << 2 | x_p << 4 | al_j << 6 |
-// al_p << 8: its class cls(k_j, k_p) depends on the two keys only and is symmetric in them
-// (exchanging the roles of b and c relabels the same digraph; the LUT gives the minimum isomorph).
-// With N[k] = #{q > i : key k} (counted when codes[] is built):
-//   * R[q] lies in N[k'] - [k_q = k'] - #{induced neighbours of R[q] beyond i with key k'} such
-//     sets of class cls(k_q, k') for every key k' -- one atomic per key present;
-//   * r and a lie in N[k] N[k'] (k < k') or C(N[k], 2) (k = k') sets of class cls(k, k'), minus
-//     the pairs with an R[j]-R[p] edge (E[k][k'], counted below) -- added once per task;
-//   * a pair with an R[j]-R[p] edge (an event: an entry of the root's induced adjacency, k_nr) is
-//     classified alone by its full mask, code(R[j], R[p]) in bits 10-11.
+// ------------------------------------- shapes "3" and "2+1" at heavy roots, counted in closed form
+// Task (r, x = R[i]), Y = code(r, x).  The key of a position q != i is codes[q] = x_q | al_q << 2
+// with x_q = code(r, R[q]) and al_q = code(x, R[q]); N[k] = #{q > i : key k}, N[16 + k] =
+// #{q < i : key k} (counted when codes[] is built), M[w] = #{c in L_x : code(x, c) = w}.
+//
+// "3" = {r, x, R[j], R[p]}, i < j < p.  A pair (j, p) with no R[j]-R[p] edge has the mask
+// Y | x_j << 2 | x_p << 4 | al_j << 6 | al_p << 8: its class cls(k_j, k_p) depends on the two keys
+// only and is symmetric in them (exchanging the roles of b and c relabels the same digraph; the
+// LUT gives the minimum isomorph).  So
+//   * R[q] (q > i) lies in N[k'] - [k_q = k'] - #{induced neighbours of R[q] beyond i with key k'}
+//     such sets of class cls(k_q, k') -- one atomic per key present;
+//   * r and x lie in N[k] N[k'] (k < k') or C(N[k], 2) (k = k') sets of class cls(k, k');
+//   * a pair with an R[j]-R[p] edge (an entry of the root's induced adjacency, k_nr) is an event:
+//     classified alone by its full mask (code(R[j], R[p]) in bits 10-11) and taken back from its
+//     plain class.
+// "2+1" with x as a depth-1 vertex (the partition of the enumerated cross items):
+//   PART 1, j > i: {r, a = x, b = R[j], c}, c in L_x, every j:  mask Y | x_j << 2 | al_j << 6 |
+//                  w_c << 8 | code(R[j], c) << 10
+//   PART 2, j < i: {r, a = R[j], b = x, c}, c in L_x, c not adjacent to R[j]:  mask x_j | Y << 2 |
+//                  swap(al_j) << 6 | w_c << 10
+// With no R[j]-c edge the class depends on (k_j, w_c, part) only: c lies in N[k] (part 1) /
+// N[16 + k] (part 2) sets per key, R[j] in M[w] sets per w, r and x in M[w] N[..k] sets; every
+// R[j]-c edge (walked from c's list) is an event of part 1 (classified alone) or removes a part-2
+// set, and is taken back from the plain counts.
 // The induced graph of N+(r) is sparse (cfg4: 51K edges over all 6585 heavy roots), so a task
-// costs O(D - i) plus its events instead of O((D - i)^2) set visits; every set is still counted
-// once, in the class of its exact mask.
-constexpr int kSPM = 2;                 // positions per lane in one closed-form star item
+// costs O(D + sum of |N(c)| over c in L_x) plus its events instead of O((D - i)^2 + |L_x| D) set
+// visits; every set is still counted once, in the class of its exact mask.
+// Take-backs make some partial sums negative: the r / x side of the events and take-backs goes to
+// the per-CTA histogram Hs of modular 64-bit words, flushed once per task (closed_root).
+constexpr int kSPM = 2;                 // positions per lane in one closed-form item
 constexpr int kSPW = 32 * kSPM;
 
-__device__ __forceinline__ void acc_addw(AccT *p, AccT v) { atomicAdd(p, v); }   // modular (v may be "-1")
+__device__ __forceinline__ void acc_addw(AccT *p, AccT v) { atomicAdd(p, v); }   // modular ("-1" = all ones)
+__device__ __forceinline__ void hs_add(unsigned long long *Hs, uint32_t col, long long v) {
+    atomicAdd(Hs + col, (unsigned long long)v);
+}
+__device__ __forceinline__ uint32_t star_mask(uint32_t cra, uint32_t kb, uint32_t kc) {   // plain "3" mask
+    return cra | (kb & 3u) << 2 | (kc & 3u) << 4 | (kb >> 2) << 6 | (kc >> 2) << 8;
+}
+__device__ __forceinline__ uint32_t p1_mask(uint32_t cra, uint32_t kj, uint32_t w) {   // plain "2+1" part 1
+    return cra | (kj & 3u) << 2 | (kj >> 2) << 6 | w << 8;
+}
+__device__ __forceinline__ uint32_t p2_mask(uint32_t cra, uint32_t kj, uint32_t w) {   // plain "2+1" part 2
+    return (kj & 3u) | cra << 2 | swap2(kj >> 2) << 6 | w << 10;
+}
 
+// "3": positions [q0, q0 + kSPW) beyond i, one per lane
 template <int C>
-__device__ __forceinline__ void star_closed_item(const Dev &g, const uint8_t *lut, uint32_t *H, uint32_t cra, int i,
-                                                 const uint32_t *R, int D, const uint8_t *codes, const int *sN,
-                                                 int *sE, uint32_t P, int64_t seg, int q0, int lane) {
+__device__ __forceinline__ void star_closed_item(const Dev &g, const uint8_t *lut, unsigned long long *Hs,
+                                                 uint32_t cra, int i, const uint32_t *R, int D,
+                                                 const uint8_t *codes, const int *sN, uint32_t P, int64_t seg,
+                                                 int q0, int lane) {
 #pragma unroll 1
     for (int t = 0; t < kSPM; t++) {
         const int q = q0 + 32 * t + lane;
         if (q >= D) break;   // no warp-collective operations below
         const uint32_t v = R[q] >> 2, kq = codes[q];
-        const uint32_t mq = cra | (kq & 3u) << 2 | (kq >> 2) << 6;   // R[q] in the b slots
         uint64_t corr = 0;   // induced neighbours beyond i with keys 1..3 (al = 0), 21-bit fields
         int64_t e = g.nr_off[seg + q];
         const int64_t e1 = g.nr_off[seg + q + 1];
@@ -606,43 +632,121 @@ __device__ __forceinline__ void star_closed_item(const Dev &g, const uint8_t *lu
             const int p = (int)(en >> 2);
             if (p <= i) continue;
             const uint32_t kp = codes[p];
-            const uint32_t mp = mq | (kp & 3u) << 4 | (kp >> 2) << 8;
+            const uint32_t mp = star_mask(cra, kq, kp);
             if (kp < 4u) corr += 1ull << (21u * (kp - 1u));
-            else acc_addw(accp(g, v, lut[mp]), (AccT)0 - (AccT)1);   // not plain: take it back from below
-            if (p > q) {   // the event set {r, a, R[q], R[p]}, R[q] in the b slots
-                const uint32_t col = lut[mp | (en & 3u) << 10];
+            else acc_addw(accp(g, v, lut[mp]), (AccT)0 - (AccT)1);   // not plain: taken back from below
+            if (p > q) {   // the event {r, x, R[q], R[p]}, R[q] in the b slots
+                const uint32_t col = lut[mp | (en & 3u) << 10], pl = lut[mp];
                 acc_add(accp(g, v, col), 1u);
-                acc_add(accp(g, R[p] >> 2, col), 1u);
-                atomicAdd(H + col, 1u);
-                atomicAdd(sE + (min(kq, kp) << 4 | max(kq, kp)), 1);
+                acc_add(accp(g, R[p] >> 2, col), 1u);   // (R[p]'s own walk takes it back from its plain sets)
+                hs_add(Hs, col, 1);
+                hs_add(Hs, pl, -1);
             }
         }
         for (uint32_t m = P; m; m &= m - 1u) {   // plain sets of R[q], per partner key
             const uint32_t k = (uint32_t)__ffs(m) - 1u;
             uint32_t cnt = (uint32_t)sN[k] - (k == kq ? 1u : 0u);
             if (k < 4u) cnt -= (uint32_t)(corr >> (21u * (k - 1u))) & 0x1fffffu;
-            if (cnt) acc_add(accp(g, v, lut[mq | (k & 3u) << 4 | (k >> 2) << 8]), cnt);
+            if (cnt) acc_add(accp(g, v, lut[star_mask(cra, kq, k)]), cnt);
         }
     }
 }
 
-// r and a: the plain pairs of every key pair, once per task (thread tid < 256: keys tid >> 4 <= tid & 15)
+// "2+1", the R[j] side: positions j in [q0, q0 + kSPW), j != i, one per lane: M[w] sets per w
 template <int C>
-__device__ __forceinline__ void star_closed_root(const Dev &g, const uint8_t *lut, uint32_t r, uint32_t a,
-                                                 uint32_t cra, int *sN, int *sE, int tid) {
-    if (tid >= 256) return;
-    const uint32_t k1 = (uint32_t)tid >> 4, k2 = (uint32_t)tid & 15u;
-    const int e = sE[tid];
-    if (k1 <= k2 && (k1 & 3u) && (k2 & 3u)) {
-        const uint64_t n1 = (uint64_t)sN[k1], n2 = (uint64_t)sN[k2];
-        const uint64_t pairs = (k1 < k2 ? n1 * n2 : n1 * (n1 - (n1 > 0)) / 2) - (uint64_t)e;
-        if (pairs) {
-            const uint32_t col = lut[cra | (k1 & 3u) << 2 | (k2 & 3u) << 4 | (k1 >> 2) << 6 | (k2 >> 2) << 8];
-            acc_addw(accp(g, r, col), (AccT)pairs);
-            acc_addw(accp(g, a, col), (AccT)pairs);
+__device__ __forceinline__ void cross_j_closed(const Dev &g, const uint8_t *lut, uint32_t cra, int i,
+                                               const uint32_t *R, int D, const uint8_t *codes, const int *sM,
+                                               int q0, int lane) {
+#pragma unroll 1
+    for (int t = 0; t < kSPM; t++) {
+        const int j = q0 + 32 * t + lane;
+        if (j >= D) break;
+        if (j == i) continue;
+        const uint32_t y = R[j] >> 2, kj = codes[j];
+#pragma unroll
+        for (uint32_t w = 1; w <= 3; w++) {
+            const uint32_t mw = (uint32_t)sM[w];
+            if (mw) acc_add(accp(g, y, lut[j > i ? p1_mask(cra, kj, w) : p2_mask(cra, kj, w)]), mw);
         }
     }
-    if (e) sE[tid] = 0;
+}
+
+// "2+1", the c side: c = L_x[q] (one warp): c's R-neighbours are events (part 1) or removals
+// (part 2); then c's plain sets, lane l = (part l >> 4, key l & 15)
+template <int C>
+__device__ __forceinline__ void cross_c_closed(const Dev &g, const uint8_t *lut, unsigned long long *Hs,
+                                               uint32_t r, uint32_t cra, int i, const uint32_t *R, int D,
+                                               const uint8_t *codes, const uint32_t *La, const int *sN, int q,
+                                               int lane) {
+    const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
+    const int64_t c0 = g.off[c], c1 = g.off[c + 1];
+    for (int64_t base = c0; base < c1; base += 32) {
+        const int64_t p = base + lane;
+        if (p < c1) {
+            const uint32_t e = g.adj[p], y = e >> 2;
+            if (y > r) {
+                const int pos = find_rank(R, D, y);
+                if (pos >= 0 && pos != i) {
+                    const uint32_t kj = codes[pos];
+                    if (pos > i) {   // part-1 event: code(R[j], c) = swap(code(c, R[j]))
+                        const uint32_t mp = p1_mask(cra, kj, w);
+                        const uint32_t col = lut[mp | swap2(e & 3u) << 10], pl = lut[mp];
+                        acc_add(accp(g, c, col), 1u);
+                        acc_add(accp(g, y, col), 1u);
+                        acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                        acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                        hs_add(Hs, col, 1);
+                        hs_add(Hs, pl, -1);
+                    } else {         // part 2: c ~ R[j], the set belongs to R[j]'s task
+                        const uint32_t pl = lut[p2_mask(cra, kj, w)];
+                        acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                        acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                        hs_add(Hs, pl, -1);
+                    }
+                }
+            }
+        }
+    }
+    const uint32_t k = (uint32_t)lane & 15u;
+    const int n = sN[lane];
+    if (n > 0 && (k & 3u)) acc_add(accp(g, c, lut[lane < 16 ? p1_mask(cra, k, w) : p2_mask(cra, k, w)]), (uint32_t)n);
+}
+
+// r and x: the plain sets of every key pair ("3") and of every (key, w, part) ("2+1"), and the
+// per-CTA take-back histogram; once per task, after the items (threads tid < 256 / 96 / C)
+template <int C>
+__device__ __forceinline__ void closed_root(const Dev &g, const uint8_t *lut, uint32_t r, uint32_t x, uint32_t cra,
+                                            const int *sN, const int *sM, unsigned long long *Hs, int tid) {
+    if (tid < 256) {
+        const uint32_t k1 = (uint32_t)tid >> 4, k2 = (uint32_t)tid & 15u;
+        if (k1 <= k2 && (k1 & 3u) && (k2 & 3u)) {
+            const uint64_t n1 = (uint64_t)sN[k1], n2 = (uint64_t)sN[k2];
+            const uint64_t pairs = k1 < k2 ? n1 * n2 : n1 * (n1 - (n1 > 0)) / 2;
+            if (pairs) {
+                const uint32_t col = lut[star_mask(cra, k1, k2)];
+                acc_addw(accp(g, r, col), (AccT)pairs);
+                acc_addw(accp(g, x, col), (AccT)pairs);
+            }
+        }
+    }
+    if (tid < 96) {
+        const int part = tid / 48, rest = tid % 48;
+        const uint32_t k = (uint32_t)rest / 3u, w = (uint32_t)rest % 3u + 1u;
+        const uint64_t n = (uint64_t)sN[16 * part + (int)k] * (uint64_t)sM[w];
+        if (n && (k & 3u)) {
+            const uint32_t col = lut[part == 0 ? p1_mask(cra, k, w) : p2_mask(cra, k, w)];
+            acc_addw(accp(g, r, col), (AccT)n);
+            acc_addw(accp(g, x, col), (AccT)n);
+        }
+    }
+    if (tid < C) {
+        const unsigned long long h = Hs[tid];
+        if (h) {
+            acc_addw(accp(g, r, tid), (AccT)h);
+            acc_addw(accp(g, x, tid), (AccT)h);
+            Hs[tid] = 0;
+        }
+    }
 }
 
 // first j' in [j, jend) with an a-b edge (codes[j'] >= 4), else jend
@@ -1138,7 +1242,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
                                            int *s_ca, const Staged *st, int w, int lane, const int *sN = nullptr,
-                                           int *sE = nullptr) {
+                                           const int *sM = nullptr, unsigned long long *Hs = nullptr) {
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -1173,19 +1277,41 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         for (int x = 0; !(VDMC_SKIPF(g) & 4) && x < nL; x++)
             item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, list_at(g, La, x, st->LL, st->LS, st->lok),
                             lane, st->FR, st->FL);
+    } else if (g.fold <= 0) {
+        // closed form (default): "3" items (positions beyond i), "2+1" R[j]-side items (all
+        // positions), "2+1" c items (one per c in L_x), then the enumerated b-in-L_a items
+        const int rem = D - i - 1;
+        const int nstar = rem >= 2 ? (rem + kSPW - 1) / kSPW : 0;
+        const int nj = (VDMC_SKIPF(g) & 2) || nL == 0 ? 0 : (D + kSPW - 1) / kSPW;
+        const int nc = (VDMC_SKIPF(g) & 2) ? 0 : nL;
+        const int total = nstar + nj + nc + nL;
+        const uint32_t P = __ballot_sync(kFull, lane < 16 && sN[lane] > 0);   // keys present beyond i
+        const int64_t seg = g.hbase[r];
+        for (;;) {
+            int it = 0;
+            if (lane == 0) it = atomicAdd(wctr, 1);
+            it = __shfl_sync(kFull, it, 0);
+            if (it >= total) break;
+            if (it < nstar) {
+                if (!(VDMC_SKIPF(g) & 1)) star_closed_item<C>(g, lut, Hs, cra, i, R, D, codes, sN, P, seg, i + 1 + it * kSPW, lane);
+            } else if (it < nstar + nj) {
+                cross_j_closed<C>(g, lut, cra, i, R, D, codes, sM, (it - nstar) * kSPW, lane);
+            } else if (it < nstar + nj + nc) {
+                cross_c_closed<C>(g, lut, Hs, r, cra, i, R, D, codes, La, sN, it - nstar - nj, lane);
+            } else if (!(VDMC_SKIPF(g) & 4)) {
+                const int x = it - nstar - nj - nc;
+                item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, glist(g, La[x] >> 2), lane);
+            }
+            __syncwarp();
+        }
     } else {
+        // enumerated path (star_block option): star chunk items, cross items over CA lists
         uint32_t *CAbeg = ca, *CAlen = ca + g.maxdeg, *CA = ca + 2 * (int64_t)g.maxdeg;
         const bool cross = !(VDMC_SKIPF(g) & 8) && ca_build<NW>(g, r, i, R, D, La, nL, CAbeg, CAlen, CA, s_ca, w, lane);
-        // shape "3": closed form (default), or the enumerated star items when the star_block option
-        // is given (chunk x block of b positions; kept as the per-set reference path)
-        const bool closed = g.fold <= 0;
-        const int fold = closed ? kMaxBlock : g.fold;
+        const int fold = g.fold;
         const int nch = D - (i + 2) > 0 ? (D - (i + 2) + kStarW - 1) / kStarW : 0;   // star chunks
         int nstar = 0;
-        if (closed) nstar = D - (i + 2) > 0 ? (D - (i + 1) + kSPW - 1) / kSPW : 0;
-        else
-            for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
-        const uint32_t P = __ballot_sync(kFull, closed && lane < 16 && sN[lane] > 0);   // keys present beyond i
+        for (int kk = 0; kk < nch; kk++) nstar += star_blocks(D, i, kk, fold);
         const int nck = (nL + kStarW - 1) / kStarW, njb = (D + g.xblock - 1) / g.xblock;
         const int nB = cross ? nck * njb : nL;                                  // "2+1" items
         const int total = nstar + nB + nL;
@@ -1196,13 +1322,6 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
             int star_k = -1, star_b = 0, b_it = -1;
-            if (it < nstar && closed) {
-                if (!(VDMC_SKIPF(g) & 1))
-                    star_closed_item<C>(g, lut, H, cra, i, R, D, codes, sN, sE, P, g.hbase[r], i + 1 + it * kSPW, lane);
-                if (g.big) flush_hist<C>(H, g, r, a, lane);
-                __syncwarp();
-                continue;
-            }
             if (it < nstar) {
                 int rem = it, kk = 0;
                 for (;; kk++) {
@@ -1241,11 +1360,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item, s_sub[4];   // s_sub: the slice's heavy_task [h0, h1) and light_root [l0, l1)
     __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
-    __shared__ int s_N[16], s_E[256];       // closed-form star: keys beyond i, event pairs per key pair
+    __shared__ int s_N[32], s_M[4];         // closed forms: key counts beyond / before i, |L_x| per code(x, c)
+    __shared__ unsigned long long Hs[C];    // closed forms: r / x side of events and take-backs (modular)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     for (int q = tid; q < NM; q += kBlock) lut[q] = lut_g[q];
-    if (tid < 256) s_E[tid] = 0;
-    if (tid < 16) s_N[tid] = 0;
+    if (tid < C) Hs[tid] = 0;
+    if (tid < 32) s_N[tid] = 0;
+    if (tid < 4) s_M[tid] = 0;
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;
     uint32_t *H = sm + L.hist + wid * C;
     if (tid < 4) {   // both lists ascend with the task id, so the slice [lo, hi) is a sub-list of each
@@ -1306,7 +1427,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 s_ca[0] = 0;
                 s_ca[1] = 0;
             }
-            if (K == 4)   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2; s_N = key counts beyond i
+            if (K == 4) {   // codes[j] = code(r, R[j]) | code(a, R[j]) << 2; key counts s_N, s_M
+                const bool closed = g.fold <= 0;
                 for (int base = wid * 32; base < D; base += kBlock) {
                     const int q = base + lane;
                     uint32_t key = 0;
@@ -1314,19 +1436,30 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                         key = (R[q] & 3u) | get2(Ba, q) << 2;
                         codes[q] = (uint8_t)key;
                     }
-                    const bool cnt = q > i && q < D;
-                    const unsigned m = __match_any_sync(kFull, cnt ? key : 0u);
-                    if (cnt && lane == __ffs(m) - 1) atomicAdd(s_N + key, __popc(m));
+                    if (closed) {   // slot key (beyond i) or 16 + key (before i)
+                        const uint32_t slot = q < D && q != i ? key | (q < i ? 16u : 0u) : 0u;
+                        const unsigned m = __match_any_sync(kFull, slot);
+                        if (slot && lane == __ffs(m) - 1) atomicAdd(s_N + slot, __popc(m));
+                    }
                 }
+                if (closed)
+                    for (int base = wid * 32; base < nL; base += kBlock) {
+                        const int q = base + lane;
+                        const uint32_t w = q < nL ? La[q] & 3u : 0u;
+                        const unsigned m = __match_any_sync(kFull, w);
+                        if (w && lane == __ffs(m) - 1) atomicAdd(s_M + w, __popc(m));
+                    }
+            }
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_E);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
-            if (K == 4 && g.fold <= 0) star_closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_E, tid);
+            if (K == 4 && g.fold <= 0) closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_M, Hs, tid);
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
             __syncthreads();
-            if (tid < 16) s_N[tid] = 0;
+            if (tid < 32) s_N[tid] = 0;
+            if (tid < 4) s_M[tid] = 0;
         }
     }
     __syncthreads();
