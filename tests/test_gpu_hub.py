@@ -73,10 +73,14 @@ def test_cfg4_hub_roots_identity_order(vd, oracle_mod):
         lo, hi = gr.root_range(r, r + 1)
         assert hi - lo == fwd[r]
         got[r] = gr.count(4, work=(lo, hi)).cpu().numpy().view(np.uint64)
-        # the same slice with every forced path option: still the same partial
-        alt = gr.count(4, work=(lo, hi), options={"heavy_global": 1, "ca_capacity": 4096, "force_big": 1,
-                                                  "star_block": 300, "cross_block": 100})
-        assert np.array_equal(alt.cpu().numpy().view(np.uint64), got[r]), r
+        # the same slice with the forced path options: the enumerated heavy path (every set
+        # visited, 1023-wide star blocks; and with every fallback forced) and the closed form with
+        # global buffers and per-item flushes: still the same partial
+        for opts in ({"star_block": 1023},
+                     {"heavy_global": 1, "ca_capacity": 4096, "force_big": 1, "star_block": 300, "cross_block": 100},
+                     {"heavy_global": 1, "force_big": 1}):
+            alt = gr.count(4, work=(lo, hi), options=opts)
+            assert np.array_equal(alt.cpu().numpy().view(np.uint64), got[r]), (r, opts)
     gr.close()
     for t in th:
         t.join()

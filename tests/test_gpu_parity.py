@@ -89,13 +89,16 @@ def test_rank_invariance(vd, oracle_mod, k):
 
 
 PATH_MODES = {   # result-preserving path options (vdmc_count_options) forced on a small graph
-    "smem": {}, "random-rank": {},
+    "smem": {}, "random-rank": {},                  # default: heavy "3" / "2+1" sets in closed form
     "global": {"heavy_global": 1},                  # heavy buffers in global memory
-    "fold": {"star_block": 37},                     # star items of 37 b positions (default 1023)
-    "xblock": {"cross_block": 32},                  # "2+1" cross items of 32 positions (default 256)
     "big": {"force_big": 1},                        # per-item histogram flushes (max degree > 32767)
-    "ca0": {"ca_capacity": 1},                      # every heavy task: per-c "2+1" fallback items
+    # the enumerated heavy path (star_block > 0): every set visited, per-set reference of the closed form
+    "fold": {"star_block": 37},                     # star items of 37 b positions
+    "enum": {"star_block": 1023},                   # star items of 1023 b positions (widest block)
+    "xblock": {"star_block": 1023, "cross_block": 32},   # "2+1" cross items of 32 positions (default 256)
+    "ca0": {"star_block": 1023, "ca_capacity": 1},  # every heavy task: per-c "2+1" fallback items
     "all": {"heavy_global": 1, "star_block": 5, "cross_block": 33, "force_big": 1, "ca_capacity": 7},
+    "closed-all": {"heavy_global": 1, "force_big": 1},
 }
 
 
@@ -151,7 +154,7 @@ def test_ca_overflow_mixed(vd, oracle_mod, k):
     assert (needs > cap).sum() > 10 and ((needs > 0) & (needs <= cap)).sum() > 10
     want = oracle_mod.count_esu(g, k)
     for c in (cap, max(1, cap // 4)):
-        assert np.array_equal(gpu_count(vd, g, k, options={"ca_capacity": c}), want), c
+        assert np.array_equal(gpu_count(vd, g, k, options={"ca_capacity": c, "star_block": 1023}), want), c
 
 
 @pytest.mark.parametrize("k", [3, 4])

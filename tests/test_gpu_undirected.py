@@ -44,10 +44,11 @@ def test_small_fixtures(vd, oracle_mod, k):
 
 
 @pytest.mark.parametrize("k", [3, 4])
-@pytest.mark.parametrize("mode", ["smem", "global", "random-rank", "all"])
+@pytest.mark.parametrize("mode", ["smem", "global", "random-rank", "all", "enum"])
 def test_heavy_and_light_paths(vd, oracle_mod, k, mode):
     g = G.make_config("cfg3", scale=0.03)
-    opts = {"global": {"heavy_global": 1},
+    opts = {"global": {"heavy_global": 1, "force_big": 1},
+            "enum": {"star_block": 1023},   # the enumerated heavy path (default: closed form)
             "all": {"star_block": 5, "cross_block": 33, "force_big": 1, "ca_capacity": 7}}.get(mode)
     rank = np.random.default_rng(5).permutation(g[0]) if mode == "random-rank" else None
     assert np.array_equal(ucount(vd, g, k, rank=rank, options=opts), oracle_mod.count_undirected(g, k))
