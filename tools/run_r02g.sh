@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 timeout 900 python bench.py > $O/bench_cfg4.json 2> $O/bench_cfg4.err
 timeout 900 python bench.py --config cfg5 --no-cpu-baseline > $O/bench_cfg5.json 2> $O/bench_cfg5.err
-timeout 600 python tools/ab_options.py cfg4 '{}' '{"acc64": 1}' > $O/ab_acc_cfg4.txt 2>&1
+timeout 600 python tools/ab_options.py cfg4 "{}" "{\"star_block\": 1023}" > $O/ab_closed_cfg4.txt 2>&1
 timeout 600 python tools/ab_options.py cfg5 '{}' '{"acc64": 1}' > $O/ab_acc_cfg5.txt 2>&1
 timeout 600 python tools/profile_enum.py cfg2 5 2 > $O/k5_cfg2.txt 2>&1
 timeout 3000 python -m pytest tests -m gpu -q -rf --durations=25 > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
