@@ -119,7 +119,7 @@ constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
 constexpr int kPool = 896;                   // light: staged list entries, R's lists then L_a's lists
 constexpr int kFW = 32;                      // light: 1024-bit membership filters of R and of L_a
-constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool + 2 * kFW;
+constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool + 2 * kFW + 4;   // + M[4] (closed form)
 
 // accumulator element (v, col) at col * n + v.  Class-major: the updates of one class from many
 // sets share sectors with other vertices' updates of the same (hot) class, so a matrix far
@@ -210,15 +210,19 @@ __device__ __forceinline__ void emit3(uint32_t *H, const Dev &g, uint32_t b, int
     red_shared_if(v && lane == __ffs(m) - 1, H + cc, (uint32_t)__popc(m));
 }
 
-// warp-private histogram -> rows r and a
+__device__ __forceinline__ void acc_addw(AccT *p, AccT v) { atomicAdd(p, v); }   // modular ("-1" = all ones)
+
+// warp-private histogram -> rows r and a (entries are signed 32-bit: |net count| < 2^31 between
+// flushes -- per task below degree 32767, per work item above it)
 template <int C>
 __device__ __forceinline__ void flush_hist(uint32_t *H, const Dev &g, uint32_t r, uint32_t a, int lane) {
     __syncwarp();
     for (int j = lane; j < C; j += 32) {
         const uint32_t v = H[j];
-        if (v) {
-            acc_add(accp(g, r, j), v);
-            acc_add(accp(g, a, j), v);
+        if (v) {   // signed: the closed forms' take-backs can leave a net negative entry in a warp
+            const AccT sv = (AccT)(long long)(int)v;
+            acc_addw(accp(g, r, j), sv);
+            acc_addw(accp(g, a, j), sv);
             H[j] = 0;
         }
     }
@@ -590,7 +594,6 @@ __device__ __forceinline__ void star_fast_any(const Dev &g, const uint32_t *R, S
 constexpr int kSPM = 2;                 // positions per lane in one closed-form item
 constexpr int kSPW = 32 * kSPM;
 
-__device__ __forceinline__ void acc_addw(AccT *p, AccT v) { atomicAdd(p, v); }   // modular ("-1" = all ones)
 __device__ __forceinline__ void hs_add(unsigned long long *Hs, uint32_t col, long long v) {
     atomicAdd(Hs + col, (unsigned long long)v);
 }
@@ -1233,6 +1236,204 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
     return *s_ca <= (int)g.ca_cap;
 }
 
+// ------------------------------------------------------------- light tasks (k = 4), closed form
+// One warp, the task (r, a = R[i]) of a light root, Y = code(r, a).  As at heavy roots: "3" (b, c
+// in R beyond i), "2+1" with c in L_a (every b in R beyond i) and "1+2" (b, c in L_a) are counted
+// from the key counts N[k] (positions beyond i) and M[w] (|L_a| per code(a, c)), with their
+// edge pairs as events (classified alone, taken back from the plain counts); the sets that need
+// a walked entry -- "2+1" with c in L_b \ N(a), and "1+1+1" -- are enumerated one per lane as
+// before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back.
+// N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
+template <int C>
+__device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *lut, uint32_t r, int i,
+                                                  const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La,
+                                                  int nL, uint32_t *H, int *N, int *M, const Staged *st, int lane) {
+    const uint32_t Y = R[i] & 3u, a = R[i] >> 2;
+    const uint32_t *FR = st->FR, *FL = st->FL;
+    if (lane < 16) N[lane] = 0;
+    if (lane < 4) M[lane] = 0;
+    __syncwarp();
+    for (int base = i + 1; base < D; base += 32) {   // one leader per distinct key: no race
+        const int q = base + lane;
+        const uint32_t key = q < D ? (R[q] & 3u) | get2(Ba, q) << 2 : 0u;
+        const unsigned m = __match_any_sync(kFull, key);
+        if (key && lane == __ffs(m) - 1) N[key] += __popc(m);
+    }
+    for (int base = 0; base < nL; base += 32) {
+        const int q = base + lane;
+        const uint32_t w = q < nL ? La[q] & 3u : 0u;
+        const unsigned m = __match_any_sync(kFull, w);
+        if (w && lane == __ffs(m) - 1) M[w] += __popc(m);
+    }
+    __syncwarp();
+    const uint32_t P = __ballot_sync(kFull, lane < 16 && N[lane] > 0);   // keys present beyond i
+    // b = R[j], j > i: walk b's list
+    for (int j = i + 1; !(VDMC_SKIPF(g) & 2) && j < D; j++) {
+        const uint32_t eb = R[j], b = eb >> 2;
+        const uint32_t kb = (eb & 3u) | get2(Ba, j) << 2;
+        const uint32_t mb = Y | (kb & 3u) << 2 | (kb >> 2) << 6;   // b in the b slots
+        const List bl = list_at(g, R, j, st->RL, st->RS, st->rok);
+        uint32_t corr = 0;   // b's induced neighbours beyond i with keys 1..3, 10-bit fields (D <= 128)
+        for (int base = 0; base < bl.len; base += 32 * kPF) {
+            uint32_t ev[kPF];
+#pragma unroll
+            for (int u = 0; u < kPF; u++) {
+                const int p = base + 32 * u + lane;
+                ev[u] = p < bl.len ? bl.p[p] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kPF; u++) {
+                if (base + 32 * u >= bl.len) break;
+                const uint32_t e = ev[u];
+                int col = kNone;
+                uint32_t c = 0;
+                if (base + 32 * u + lane < bl.len) {
+                    c = e >> 2;
+                    if (c > r) {
+                        const int pos = fmay(FR, c) ? find_rank(R, D, c) : -1;
+                        if (pos >= 0) {
+                            if (pos > i && pos != j) {   // an induced edge of the "3" sets
+                                const uint32_t kp = (R[pos] & 3u) | get2(Ba, pos) << 2;
+                                const uint32_t mp = star_mask(Y, kb, kp);
+                                if (kp < 4u) corr += 1u << (10u * (kp - 1u));
+                                else acc_addw(accp(g, b, lut[mp]), (AccT)0 - (AccT)1);
+                                if (pos > j) {   // the event {r, a, b, R[pos]}
+                                    const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                                    acc_add(accp(g, b, ce), 1u);
+                                    acc_add(accp(g, c, ce), 1u);
+                                    atomicAdd(H + ce, 1u);
+                                    atomicAdd(H + pl, 0xffffffffu);
+                                }
+                            }
+                        } else {
+                            const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
+                            if (q >= 0) {   // "2+1" with c in L_a and a b-c edge: event
+                                const uint32_t mp = p1_mask(Y, kb, La[q] & 3u);
+                                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                                acc_add(accp(g, b, ce), 1u);
+                                acc_add(accp(g, c, ce), 1u);
+                                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
+                                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                                atomicAdd(H + ce, 1u);
+                                atomicAdd(H + pl, 0xffffffffu);
+                            } else {
+                                col = lut[mb | (e & 3u) << 10];   // "2+1" with c in L_b \ N(a)
+                            }
+                        }
+                    }
+                }
+                emit4<C>(H, g, b, c, col, lane);
+            }
+        }
+        // b's plain sets: "3" per partner key (lanes 1..15), "2+1" with c in L_a per w (lanes 17..19)
+        corr = __reduce_add_sync(kFull, corr);
+        if (lane < 16) {
+            if ((P >> lane) & 1u) {
+                uint32_t cnt = (uint32_t)N[lane] - ((uint32_t)lane == kb ? 1u : 0u);
+                if (lane < 4) cnt -= (corr >> (10u * ((uint32_t)lane - 1u))) & 0x3ffu;
+                if (cnt) acc_add(accp(g, b, lut[star_mask(Y, kb, (uint32_t)lane)]), cnt);
+            }
+        } else if (lane >= 17 && lane <= 19) {
+            const uint32_t w = (uint32_t)lane - 16u;
+            if (M[w]) acc_add(accp(g, b, lut[p1_mask(Y, kb, w)]), (uint32_t)M[w]);
+        }
+        if (g.big) flush_hist<C>(H, g, r, a, lane);
+        __syncwarp();
+    }
+    // c in L_a: "2+1" plain (every b in R beyond i, per key) and "1+2" plain (partners in L_a per w)
+    if (!(VDMC_SKIPF(g) & 2))
+        for (int base = 0; base < nL; base += 32) {
+            const int q = base + lane;
+            if (q < nL) {
+                const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
+                for (uint32_t m = P; m; m &= m - 1u) {
+                    const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                    acc_add(accp(g, c, lut[p1_mask(Y, k, w)]), (uint32_t)N[k]);
+                }
+#pragma unroll
+                for (uint32_t w2 = 1; w2 <= 3; w2++) {
+                    const uint32_t cnt = (uint32_t)M[w2] - (w2 == w ? 1u : 0u);
+                    if (cnt) acc_add(accp(g, c, lut[Y | w << 6 | w2 << 8]), cnt);
+                }
+            }
+        }
+    // b = L_a[x]: "1+1+1" sets per walked entry, "1+2" edge events
+    for (int x = 0; !(VDMC_SKIPF(g) & 4) && x < nL; x++) {
+        const uint32_t eb = La[x], b = eb >> 2, wb = eb & 3u;
+        const uint32_t mb = Y | wb << 6;
+        const List bl = list_at(g, La, x, st->LL, st->LS, st->lok);
+        for (int base = 0; base < bl.len; base += 32 * kPF) {
+            uint32_t ev[kPF];
+#pragma unroll
+            for (int u = 0; u < kPF; u++) {
+                const int p = base + 32 * u + lane;
+                ev[u] = p < bl.len ? bl.p[p] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kPF; u++) {
+                if (base + 32 * u >= bl.len) break;
+                const uint32_t e = ev[u];
+                int col = kNone;
+                uint32_t c = 0;
+                if (base + 32 * u + lane < bl.len) {
+                    c = e >> 2;
+                    if (c > r && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
+                        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
+                        if (q >= 0) {
+                            if (q > x) {   // "1+2" with a b-c edge: event
+                                const uint32_t mp = mb | (La[q] & 3u) << 8;
+                                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                                acc_add(accp(g, b, ce), 1u);
+                                acc_add(accp(g, c, ce), 1u);
+                                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
+                                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                                atomicAdd(H + ce, 1u);
+                                atomicAdd(H + pl, 0xffffffffu);
+                            }
+                        } else {
+                            col = lut[mb | (e & 3u) << 10];   // "1+1+1"
+                        }
+                    }
+                }
+                emit4<C>(H, g, b, c, col, lane);
+            }
+        }
+        if (g.big) flush_hist<C>(H, g, r, a, lane);
+        __syncwarp();
+    }
+    // r and a: the plain pairs -- "3" per key pair, "2+1" with c in L_a per (key, w), "1+2" per w pair
+    for (int idx = lane; idx < 256 + 48 + 16; idx += 32) {
+        uint64_t cnt = 0;
+        uint32_t mask = 0;
+        if (idx < 256) {
+            const uint32_t k1 = (uint32_t)idx >> 4, k2 = (uint32_t)idx & 15u;
+            if (k1 <= k2 && ((P >> k1) & (P >> k2) & 1u)) {
+                const uint64_t n1 = (uint64_t)N[k1], n2 = (uint64_t)N[k2];
+                cnt = k1 < k2 ? n1 * n2 : n1 * (n1 - 1) / 2;
+                mask = star_mask(Y, k1, k2);
+            }
+        } else if (idx < 256 + 48) {
+            const uint32_t k = (uint32_t)(idx - 256) / 3u, w = (uint32_t)(idx - 256) % 3u + 1u;
+            if ((P >> k) & 1u) {
+                cnt = (uint64_t)N[k] * (uint64_t)M[w];
+                mask = p1_mask(Y, k, w);
+            }
+        } else {
+            const uint32_t w1 = (uint32_t)(idx - 304) >> 2, w2 = (uint32_t)(idx - 304) & 3u;
+            if (w1 >= 1 && w1 <= w2 && w2 <= 3) {
+                const uint64_t m1 = (uint64_t)M[w1], m2 = (uint64_t)M[w2];
+                cnt = w1 < w2 ? m1 * m2 : m1 * (m1 - (m1 > 0)) / 2;
+                mask = Y | w1 << 6 | w2 << 8;
+            }
+        }
+        if (cnt) {
+            const uint32_t col = lut[mask];
+            acc_addw(accp(g, r, col), (AccT)cnt);
+            acc_addw(accp(g, a, col), (AccT)cnt);
+        }
+    }
+}
+
 // The task (r, a = R[i]).  Ba/La (phase A) and, for heavy k = 4 tasks, codes must be ready.
 // NW == 1: one warp does everything in order.  NW > 1 (heavy): the CTA's warps take work
 // items from the shared counter *wctr (star chunks longest first, then b in R, then b in L_a).
@@ -1515,8 +1716,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 for (int q = lane; q < nL; q += 32) fadd(FL, La[q] >> 2);
                 __syncwarp();
                 st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
-                task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr, &st,
-                                    0, lane);
+                if (K == 4 && g.fold <= 0)
+                    light_task_closed<C>(g, lut, r, i, R, D, Ba, La, nL, H, reinterpret_cast<int *>(Bb),
+                                         reinterpret_cast<int *>(FL + kFW), &st, lane);
+                else
+                    task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr,
+                                        &st, 0, lane);
                 flush_hist<C>(H, g, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
