@@ -674,49 +674,89 @@ __device__ __forceinline__ void cross_j_closed(const Dev &g, const uint8_t *lut,
     }
 }
 
-// "2+1", the c side: c = L_x[q] (one warp): c's R-neighbours are events (part 1) or removals
-// (part 2); then c's plain sets, lane l = (part l >> 4, key l & 15)
+// u = L_x[q] (one warp, one walk of u's list) for every shape with a depth-2 vertex:
+//   * u as c of "2+1": an entry y = R[j] (j != i) is a part-1 event (j > i: classified alone) or
+//     a part-2 removal (j < i: the set belongs to R[j]'s task), both taken back from the plain
+//     counts; afterwards u's plain "2+1" sets per (part, key), lane l = (l >> 4, l & 15);
+//   * u as b of "1+2" / "1+1+1": an entry y in L_x after u is a "1+2" event (classified alone,
+//     taken back); an entry y outside N[r] u N[x], y > r, is a "1+1+1" set {r, x, u, y}, enumerated
+//     one per lane; afterwards u's plain "1+2" sets per partner code w2.
+// y = x (always in u's list) is in R and tested first, so that the lane holding it does not send
+// the whole warp through the binary search.
 template <int C>
-__device__ __forceinline__ void cross_c_closed(const Dev &g, const uint8_t *lut, unsigned long long *Hs,
-                                               uint32_t r, uint32_t cra, int i, const uint32_t *R, int D,
-                                               const uint8_t *codes, const uint32_t *La, const int *sN, int q,
-                                               int lane) {
-    const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
-    const int64_t c0 = g.off[c], c1 = g.off[c + 1];
-    for (int64_t base = c0; base < c1; base += 32) {
-        const int64_t p = base + lane;
-        if (p < c1) {
-            const uint32_t e = g.adj[p], y = e >> 2;
-            if (y > r) {
+__device__ __forceinline__ void u_closed(const Dev &g, const uint8_t *lut, unsigned long long *Hs, uint32_t *H,
+                                         uint32_t r, uint32_t x, uint32_t cra, int i, const uint32_t *R, int D,
+                                         const uint8_t *codes, const uint32_t *La, int nL, const int *sN,
+                                         const int *sM, int q, int lane) {
+    const uint32_t eu = La[q], u = eu >> 2, w = eu & 3u;
+    const uint32_t mb = cra | w << 6;   // u in the b slots of "1+2" / "1+1+1": (a, b) = code(x, u)
+    const int64_t u0 = g.off[u], u1 = g.off[u + 1];
+    for (int64_t base = u0; base < u1; base += 32 * kPF) {
+        uint32_t ev[kPF];
+#pragma unroll
+        for (int t = 0; t < kPF; t++) {
+            const int64_t p = base + 32 * t + lane;
+            ev[t] = p < u1 ? g.adj[p] : 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < kPF; t++) {
+            if (base + 32 * t >= u1) break;
+            const uint32_t e = ev[t], y = e >> 2;
+            int col = kNone;
+            uint32_t cy = 0;
+            if (base + 32 * t + lane < u1 && y > r && y != x) {
                 const int pos = find_rank(R, D, y);
-                if (pos >= 0 && pos != i) {
+                if (pos >= 0) {
                     const uint32_t kj = codes[pos];
-                    if (pos > i) {   // part-1 event: code(R[j], c) = swap(code(c, R[j]))
+                    if (pos > i) {   // part-1 event: code(R[j], u) = swap(code(u, R[j]))
                         const uint32_t mp = p1_mask(cra, kj, w);
-                        const uint32_t col = lut[mp | swap2(e & 3u) << 10], pl = lut[mp];
-                        acc_add(accp(g, c, col), 1u);
-                        acc_add(accp(g, y, col), 1u);
-                        acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                        const uint32_t ce = lut[mp | swap2(e & 3u) << 10], pl = lut[mp];
+                        acc_add(accp(g, u, ce), 1u);
+                        acc_add(accp(g, y, ce), 1u);
+                        acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
                         acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
-                        hs_add(Hs, col, 1);
+                        hs_add(Hs, ce, 1);
                         hs_add(Hs, pl, -1);
-                    } else {         // part 2: c ~ R[j], the set belongs to R[j]'s task
+                    } else {         // part 2: u ~ R[j], the set belongs to R[j]'s task
                         const uint32_t pl = lut[p2_mask(cra, kj, w)];
-                        acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                        acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
                         acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
                         hs_add(Hs, pl, -1);
                     }
+                } else {
+                    const int qq = find_rank(La, nL, y);
+                    if (qq >= 0) {
+                        if (qq > q) {   // "1+2" {r, x, u, y} with a u-y edge: event
+                            const uint32_t mp = mb | (La[qq] & 3u) << 8;
+                            const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                            acc_add(accp(g, u, ce), 1u);
+                            acc_add(accp(g, y, ce), 1u);
+                            acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
+                            acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                            hs_add(Hs, ce, 1);
+                            hs_add(Hs, pl, -1);
+                        }
+                    } else {
+                        col = lut[mb | (e & 3u) << 10];   // "1+1+1" {r, x, u, y}
+                        cy = y;
+                    }
                 }
             }
+            emit4<C>(H, g, u, cy, col, lane);
         }
     }
     const uint32_t k = (uint32_t)lane & 15u;
     const int n = sN[lane];
-    if (n > 0 && (k & 3u)) acc_add(accp(g, c, lut[lane < 16 ? p1_mask(cra, k, w) : p2_mask(cra, k, w)]), (uint32_t)n);
+    if (n > 0 && (k & 3u)) acc_add(accp(g, u, lut[lane < 16 ? p1_mask(cra, k, w) : p2_mask(cra, k, w)]), (uint32_t)n);
+    if (lane >= 1 && lane <= 3) {
+        const uint32_t w2 = (uint32_t)lane, cnt = (uint32_t)sM[w2] - (w2 == w ? 1u : 0u);
+        if (cnt) acc_add(accp(g, u, lut[cra | w << 6 | w2 << 8]), cnt);
+    }
 }
 
-// r and x: the plain sets of every key pair ("3") and of every (key, w, part) ("2+1"), and the
-// per-CTA take-back histogram; once per task, after the items (threads tid < 256 / 96 / C)
+// r and x: the plain sets of every key pair ("3"), of every (key, w, part) ("2+1") and of every
+// code pair (w1, w2) ("1+2"), and the per-CTA take-back histogram; once per task, after the
+// items (threads tid < 256 / 96 / 96..111 / C)
 template <int C>
 __device__ __forceinline__ void closed_root(const Dev &g, const uint8_t *lut, uint32_t r, uint32_t x, uint32_t cra,
                                             const int *sN, const int *sM, unsigned long long *Hs, int tid) {
@@ -740,6 +780,18 @@ __device__ __forceinline__ void closed_root(const Dev &g, const uint8_t *lut, ui
             const uint32_t col = lut[part == 0 ? p1_mask(cra, k, w) : p2_mask(cra, k, w)];
             acc_addw(accp(g, r, col), (AccT)n);
             acc_addw(accp(g, x, col), (AccT)n);
+        }
+    }
+    if (tid >= 96 && tid < 112) {   // "1+2": pairs of L_x per (w1 <= w2)
+        const uint32_t w1 = (uint32_t)(tid - 96) >> 2, w2 = (uint32_t)(tid - 96) & 3u;
+        if (w1 >= 1 && w1 <= w2 && w2 <= 3) {
+            const uint64_t m1 = (uint64_t)sM[w1], m2 = (uint64_t)sM[w2];
+            const uint64_t n = w1 < w2 ? m1 * m2 : m1 * (m1 - (m1 > 0)) / 2;
+            if (n) {
+                const uint32_t col = lut[cra | w1 << 6 | w2 << 8];
+                acc_addw(accp(g, r, col), (AccT)n);
+                acc_addw(accp(g, x, col), (AccT)n);
+            }
         }
     }
     if (tid < C) {
@@ -937,7 +989,7 @@ __device__ __forceinline__ void item_b_in_La(const Dev &g, const uint8_t *lut, u
             uint32_t c = 0;
             if (base + 32 * u + lane < bl.len) {
                 c = e >> 2;
-                if (c > r && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
+                if (c > r && c != a && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
                     const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
                     if (q >= 0) {
                         if (q > x) {
@@ -1377,7 +1429,9 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
                 uint32_t c = 0;
                 if (base + 32 * u + lane < bl.len) {
                     c = e >> 2;
-                    if (c > r && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
+                    // c = a (always in b's list) is in R: tested first, so that the one lane holding
+                    // it does not send the whole warp through the binary search
+                    if (c > r && c != a && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
                         const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
                         if (q >= 0) {
                             if (q > x) {   // "1+2" with a b-c edge: event
@@ -1479,13 +1533,14 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, list_at(g, La, x, st->LL, st->LS, st->lok),
                             lane, st->FR, st->FL);
     } else if (g.fold <= 0) {
-        // closed form (default): "3" items (positions beyond i), "2+1" R[j]-side items (all
-        // positions), "2+1" c items (one per c in L_x), then the enumerated b-in-L_a items
+        // closed form (default): one walk per u in L_x (the long, uneven items first), then the
+        // "3" items (positions beyond i) and the "2+1" R[j]-side items (all positions), which fill
+        // the warps' tails
         const int rem = D - i - 1;
+        const int nu = (VDMC_SKIPF(g) & 4) ? 0 : nL;
         const int nstar = rem >= 2 ? (rem + kSPW - 1) / kSPW : 0;
         const int nj = (VDMC_SKIPF(g) & 2) || nL == 0 ? 0 : (D + kSPW - 1) / kSPW;
-        const int nc = (VDMC_SKIPF(g) & 2) ? 0 : nL;
-        const int total = nstar + nj + nc + nL;
+        const int total = nu + nstar + nj;
         const uint32_t P = __ballot_sync(kFull, lane < 16 && sN[lane] > 0);   // keys present beyond i
         const int64_t seg = g.hbase[r];
         for (;;) {
@@ -1493,15 +1548,14 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             if (lane == 0) it = atomicAdd(wctr, 1);
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
-            if (it < nstar) {
-                if (!(VDMC_SKIPF(g) & 1)) star_closed_item<C>(g, lut, Hs, cra, i, R, D, codes, sN, P, seg, i + 1 + it * kSPW, lane);
-            } else if (it < nstar + nj) {
-                cross_j_closed<C>(g, lut, cra, i, R, D, codes, sM, (it - nstar) * kSPW, lane);
-            } else if (it < nstar + nj + nc) {
-                cross_c_closed<C>(g, lut, Hs, r, cra, i, R, D, codes, La, sN, it - nstar - nj, lane);
-            } else if (!(VDMC_SKIPF(g) & 4)) {
-                const int x = it - nstar - nj - nc;
-                item_b_in_La<C>(g, lut, r, x, R, D, La, nL, Bl, H, cra, a, glist(g, La[x] >> 2), lane);
+            if (it < nu) {
+                u_closed<C>(g, lut, Hs, H, r, a, cra, i, R, D, codes, La, nL, sN, sM, it, lane);
+                if (g.big) flush_hist<C>(H, g, r, a, lane);
+            } else if (it < nu + nstar) {
+                if (!(VDMC_SKIPF(g) & 1))
+                    star_closed_item<C>(g, lut, Hs, cra, i, R, D, codes, sN, P, seg, i + 1 + (it - nu) * kSPW, lane);
+            } else {
+                cross_j_closed<C>(g, lut, cra, i, R, D, codes, sM, (it - nu - nstar) * kSPW, lane);
             }
             __syncwarp();
         }
