@@ -32,7 +32,14 @@ variants = [("full", {}), ("heavy only", {"VDMC_PHASES": "1"}), ("light only", {
             ("heavy, only tasks with < 128 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "-128"}),
             ("heavy, only tasks with >= 512 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "512"}),
             ("heavy, only tasks with < 512 left", {"VDMC_PHASES": "1", "VDMC_MINREM": "-512"})]
-if len(sys.argv) > 3 and sys.argv[3] == "quick":
+if len(sys.argv) > 3 and sys.argv[3] == "closed":   # the closed-form heavy path's item kinds
+    variants = variants[:3] + [("heavy, skip star items", {"VDMC_PHASES": "1", "VDMC_SKIP": "1"}),
+                               ("heavy, skip j items", {"VDMC_PHASES": "1", "VDMC_SKIP": "2"}),
+                               ("heavy, skip u walks", {"VDMC_PHASES": "1", "VDMC_SKIP": "4"}),
+                               ("heavy, skip all items", {"VDMC_PHASES": "1", "VDMC_SKIP": "7"}),
+                               ("light, skip b-in-R walks", {"VDMC_PHASES": "2", "VDMC_SKIP": "2"}),
+                               ("light, skip b-in-L_a walks", {"VDMC_PHASES": "2", "VDMC_SKIP": "4"})]
+elif len(sys.argv) > 3 and sys.argv[3] == "quick":
     variants = variants[:3]
 elif len(sys.argv) > 3 and sys.argv[3] == "tasks":
     variants = variants[:2] + [v for v in variants if "VDMC_MINREM" in v[1]]
