@@ -112,6 +112,7 @@ struct Layout {
     int hist;                     // per-warp u32 histograms [kWarps][C]
     int light;                    // light region: per warp kLightWords
     int total;                    // words
+    int T;                        // heavy: bucket index of R (u16 positions, kBuckets + 1 of them), or -1
 };
 constexpr int kLW = kLightDeg;               // light list capacity
 constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
@@ -153,6 +154,49 @@ __device__ __forceinline__ int find_rank(const uint32_t *S, int len, uint32_t x)
         else hi = mid;
     }
     return (lo < len && (S[lo] >> 2) == x) ? lo : -1;
+}
+
+// Heavy roots: a bucket index over R's vertex range (R ascends): bucket b holds the positions
+// [T[b], T[b + 1]) whose vertex v has (v - lo) >> shift == b; a lookup is one table read plus a
+// binary search over ~D / kBuckets entries instead of log2(D) steps over all of R.
+constexpr int kBuckets = 4096;
+struct RIndex {
+    uint32_t lo, hi;   // vertex range of R
+    int shift;         // bucket width 2^shift
+    const uint16_t *T; // nullptr: plain binary search
+};
+__device__ __forceinline__ int find_pos(const uint32_t *R, int D, uint32_t x, const RIndex &ix) {
+    if (!ix.T) return find_rank(R, D, x);
+    if (x < ix.lo || x > ix.hi) return -1;
+    const uint32_t b = (x - ix.lo) >> ix.shift;
+    int lo = ix.T[b], hi = ix.T[b + 1];
+    const uint32_t key = x << 2;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (R[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < ix.T[b + 1] && (R[lo] >> 2) == x) ? lo : -1;
+}
+// build T for the staged R (whole CTA; the caller syncs before use).  Returns the index.
+__device__ __forceinline__ RIndex build_rindex(const uint32_t *R, int D, uint16_t *T, int tid, int nthreads) {
+    RIndex ix{0u, 0u, 0, nullptr};
+    if (T == nullptr || D <= 0 || D > 65535) return ix;
+    ix.lo = R[0] >> 2;
+    ix.hi = R[D - 1] >> 2;
+    const uint32_t span = ix.hi - ix.lo;   // buckets 0 .. span >> shift
+    int sh = 0;
+    while ((span >> sh) >= (uint32_t)kBuckets) sh++;
+    ix.shift = sh;
+    const int nb = (int)(span >> sh) + 1;   // <= kBuckets
+    for (int q = tid; q < D; q += nthreads) {   // T[b] = first q with bucket(R[q]) >= b
+        const int bq = (int)(((R[q] >> 2) - ix.lo) >> sh);
+        const int bp = q > 0 ? (int)(((R[q - 1] >> 2) - ix.lo) >> sh) : -1;
+        for (int b = bp + 1; b <= bq; b++) T[b] = (uint16_t)q;
+    }
+    for (int b = nb + tid; b <= kBuckets; b += nthreads) T[b] = (uint16_t)D;   // past the last bucket
+    ix.T = T;
+    return ix;
 }
 
 __device__ __forceinline__ uint32_t swap2(uint32_t c) { return ((c & 1u) << 1) | (c >> 1); }
@@ -345,7 +389,7 @@ __device__ int build_a(uint32_t r, List al, const uint32_t *R, int D, uint32_t *
 // tmp: 2 * ceil(len / 32) words of scratch.  *s_nL = |L_a|.  Ends with a barrier.
 template <int NW>
 __device__ void build_a_cta(uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La, uint32_t *tmp,
-                            int *s_nL, int wid, int lane) {
+                            int *s_nL, int wid, int lane, const RIndex &ix) {
     const int G = (al.len + 31) >> 5;
     uint32_t *KM = tmp, *KO = tmp + G;
     for (int gi = wid; gi < G; gi += NW) {
@@ -354,7 +398,7 @@ __device__ void build_a_cta(uint32_t r, List al, const uint32_t *R, int D, uint3
         if (p < al.len) {
             const uint32_t e = al.p[p], x = e >> 2;
             if (x > r) {
-                const int pos = find_rank(R, D, x);
+                const int pos = find_pos(R, D, x, ix);
                 if (pos >= 0) set2(Ba, pos, e & 3u);
                 else keep = true;
             }
@@ -687,7 +731,7 @@ template <int C>
 __device__ __forceinline__ void u_closed(const Dev &g, const uint8_t *lut, unsigned long long *Hs, uint32_t *H,
                                          uint32_t r, uint32_t x, uint32_t cra, int i, const uint32_t *R, int D,
                                          const uint8_t *codes, const uint32_t *La, int nL, const int *sN,
-                                         const int *sM, int q, int lane) {
+                                         const int *sM, int q, int lane, const RIndex &ix) {
     const uint32_t eu = La[q], u = eu >> 2, w = eu & 3u;
     const uint32_t mb = cra | w << 6;   // u in the b slots of "1+2" / "1+1+1": (a, b) = code(x, u)
     const int64_t u0 = g.off[u], u1 = g.off[u + 1];
@@ -705,7 +749,7 @@ __device__ __forceinline__ void u_closed(const Dev &g, const uint8_t *lut, unsig
             int col = kNone;
             uint32_t cy = 0;
             if (base + 32 * t + lane < u1 && y > r && y != x) {
-                const int pos = find_rank(R, D, y);
+                const int pos = find_pos(R, D, y, ix);
                 if (pos >= 0) {
                     const uint32_t kj = codes[pos];
                     if (pos > i) {   // part-1 event: code(R[j], u) = swap(code(u, R[j]))
@@ -1497,7 +1541,8 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                                            int D, const uint32_t *Ba, const uint32_t *La, int nL, uint32_t *Bb,
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
                                            int *s_ca, const Staged *st, int w, int lane, const int *sN = nullptr,
-                                           const int *sM = nullptr, unsigned long long *Hs = nullptr) {
+                                           const int *sM = nullptr, unsigned long long *Hs = nullptr,
+                                           const RIndex *ix = nullptr) {
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -1549,7 +1594,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
             it = __shfl_sync(kFull, it, 0);
             if (it >= total) break;
             if (it < nu) {
-                u_closed<C>(g, lut, Hs, H, r, a, cra, i, R, D, codes, La, nL, sN, sM, it, lane);
+                u_closed<C>(g, lut, Hs, H, r, a, cra, i, R, D, codes, La, nL, sN, sM, it, lane, *ix);
                 if (g.big) flush_hist<C>(H, g, r, a, lane);
             } else if (it < nu + nstar) {
                 if (!(VDMC_SKIPF(g) & 1))
@@ -1654,6 +1699,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         }
         __syncthreads();
         int64_t staged = -1;
+        RIndex rix{0u, 0u, 0, nullptr};
         for (;;) {   // bounds re-read from shared memory (keeps them out of the loop's registers)
             if (tid == 0) s_item = s_sub[0] + (int64_t)atomicAdd(ctr, 1ull);
             __syncthreads();
@@ -1672,9 +1718,12 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
                 staged = r;
                 __syncthreads();
+                rix = build_rindex(R, D, L.T >= 0 && g.fold <= 0 ? reinterpret_cast<uint16_t *>(hb + L.T) : nullptr,
+                                   tid, kBlock);
+                __syncthreads();
             }
             const List al = glist(g, R[i] >> 2);
-            build_a_cta<kWarps>(r, al, R, D, Ba, La, hb + L.Bl, &s_nL, wid, lane);
+            build_a_cta<kWarps>(r, al, R, D, Ba, La, hb + L.Bl, &s_nL, wid, lane, rix);
             const int nL = s_nL;
             for (int q = tid; q < 2 * ((al.len + 31) >> 5); q += kBlock) hb[L.Bl + q] = 0;   // build_a_cta scratch
             if (tid == 0) {
@@ -1707,7 +1756,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             }
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs, &rix);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
             if (K == 4 && g.fold <= 0) closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_M, Hs, tid);
@@ -1969,7 +2018,8 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
     L.Ba = L.La + md;
     L.Bb = L.Ba + L.bw;                  // heavy: the per-task code bytes (md bytes)
     L.Bl = L.Bb + (md + 3) / 4;
-    const int heavy_words = L.Bl + kWarps * L.lw;
+    L.T = L.Bl + kWarps * L.lw;          // bucket index of R: (kBuckets + 1) u16
+    const int heavy_words = L.T + (kBuckets + 2) / 2;
     const int light_words = kWarps * kLightWords;
     const int hist_words = kWarps * C;
     const int budget_words = (104 * 1024) / 4 - hist_words;   // keep 2 CTAs per SM
