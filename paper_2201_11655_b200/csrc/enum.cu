@@ -1340,6 +1340,51 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
 // a walked entry -- "2+1" with c in L_b \ N(a), and "1+1+1" -- are enumerated one per lane as
 // before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back.
 // N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
+// one set with members r, a (histogram H), b (per lane: the owner of the walked entry) and c (lane):
+// b-side atomics merged over the lanes with the same (owner, column)
+template <int C>
+__device__ __forceinline__ void emit4v(uint32_t *H, const Dev &g, uint32_t b, int owner, uint32_t c, int col,
+                                       int lane) {
+    const bool v = col != kNone;
+    const uint32_t cc = v ? (uint32_t)col : 0u;
+    red_if(v, accp(g, c, cc), 1u);
+    const unsigned m = __match_any_sync(kFull, v ? ((uint32_t)owner << 8 | cc) : 0xffffffffu);
+    const bool lead = v && lane == __ffs(m) - 1;
+    const uint32_t cnt = __popc(m);
+    red_shared_if(lead, H + cc, cnt);
+    red_if(lead, accp(g, b, cc), cnt);
+}
+
+// Flattened walk over the staged lists q in [q0, q1) (pool entries [S[q0], S[q1]), every list
+// non-empty): 32 consecutive entries per pass whatever the list lengths, so short lists do not
+// leave lanes idle.  The owner of entry f is q0 + #{q in (q0, q1) : S[q] <= f}: per pass the
+// lanes load the next 32 list starts, and a bitmap of the starts inside (base, base + 32] gives
+// each lane its owner with one popc.  fn(owner, entry, valid) is called by every lane.
+template <typename Fn>
+__device__ __forceinline__ void flat_walk(const uint32_t *pool, const uint32_t *S, int q0, int q1, int lane, Fn fn) {
+    const int f1 = (int)S[q1];
+    int o = q0;
+    for (int base = (int)S[q0]; base < f1; base += 32) {
+        const int qb = o + 1 + lane;
+        const int d = qb < q1 ? (int)S[qb] - base : 64;   // start of list qb, relative to base
+        const unsigned B = __reduce_or_sync(kFull, d >= 1 && d <= 32 ? 1u << (d - 1) : 0u);
+        const int owner = o + __popc(B & ((1u << lane) - 1u));
+        const int f = base + lane;
+        const bool valid = f < f1;
+        fn(owner, valid ? pool[f] : 0u, valid);
+        o += __popc(B);
+    }
+}
+
+// ------------------------------------------------------------- light tasks (k = 4), closed form
+// One warp, the task (r, a = R[i]) of a light root, Y = code(r, a).  As at heavy roots: "3" (b, c
+// in R beyond i), "2+1" with c in L_a (every b in R beyond i) and "1+2" (b, c in L_a) are counted
+// from the key counts N[k] (positions beyond i) and M[w] (|L_a| per code(a, c)), with their
+// edge pairs as events (classified alone, taken back from the plain counts); the sets that need
+// a walked entry -- "2+1" with c in L_b \ N(a), and "1+1+1" -- are enumerated one per lane as
+// before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back; when
+// the lists are staged they are walked flattened (flat_walk), else list by list.
+// N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
 template <int C>
 __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *lut, uint32_t r, int i,
                                                   const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La,
@@ -1363,140 +1408,132 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
     }
     __syncwarp();
     const uint32_t P = __ballot_sync(kFull, lane < 16 && N[lane] > 0);   // keys present beyond i
-    // b = R[j], j > i: walk b's list
-    for (int j = i + 1; !(VDMC_SKIPF(g) & 2) && j < D; j++) {
+    // an entry e of b = R[j]'s list (j > i): induced edges of the "3" sets (take-back, event if
+    // beyond b), "2+1" events (c in L_a adjacent to b), else a "2+1" set with c in L_b \ N(a)
+    auto bR_entry = [&](int j, uint32_t e, bool valid, uint32_t &c) -> int {
+        c = e >> 2;
+        if (!valid || c <= r) return kNone;
         const uint32_t eb = R[j], b = eb >> 2;
         const uint32_t kb = (eb & 3u) | get2(Ba, j) << 2;
-        const uint32_t mb = Y | (kb & 3u) << 2 | (kb >> 2) << 6;   // b in the b slots
-        const List bl = list_at(g, R, j, st->RL, st->RS, st->rok);
-        uint32_t corr = 0;   // b's induced neighbours beyond i with keys 1..3, 10-bit fields (D <= 128)
-        for (int base = 0; base < bl.len; base += 32 * kPF) {
-            uint32_t ev[kPF];
-#pragma unroll
-            for (int u = 0; u < kPF; u++) {
-                const int p = base + 32 * u + lane;
-                ev[u] = p < bl.len ? bl.p[p] : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < kPF; u++) {
-                if (base + 32 * u >= bl.len) break;
-                const uint32_t e = ev[u];
-                int col = kNone;
-                uint32_t c = 0;
-                if (base + 32 * u + lane < bl.len) {
-                    c = e >> 2;
-                    if (c > r) {
-                        const int pos = fmay(FR, c) ? find_rank(R, D, c) : -1;
-                        if (pos >= 0) {
-                            if (pos > i && pos != j) {   // an induced edge of the "3" sets
-                                const uint32_t kp = (R[pos] & 3u) | get2(Ba, pos) << 2;
-                                const uint32_t mp = star_mask(Y, kb, kp);
-                                if (kp < 4u) corr += 1u << (10u * (kp - 1u));
-                                else acc_addw(accp(g, b, lut[mp]), (AccT)0 - (AccT)1);
-                                if (pos > j) {   // the event {r, a, b, R[pos]}
-                                    const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
-                                    acc_add(accp(g, b, ce), 1u);
-                                    acc_add(accp(g, c, ce), 1u);
-                                    atomicAdd(H + ce, 1u);
-                                    atomicAdd(H + pl, 0xffffffffu);
-                                }
-                            }
-                        } else {
-                            const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
-                            if (q >= 0) {   // "2+1" with c in L_a and a b-c edge: event
-                                const uint32_t mp = p1_mask(Y, kb, La[q] & 3u);
-                                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
-                                acc_add(accp(g, b, ce), 1u);
-                                acc_add(accp(g, c, ce), 1u);
-                                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
-                                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
-                                atomicAdd(H + ce, 1u);
-                                atomicAdd(H + pl, 0xffffffffu);
-                            } else {
-                                col = lut[mb | (e & 3u) << 10];   // "2+1" with c in L_b \ N(a)
-                            }
-                        }
-                    }
+        const int pos = fmay(FR, c) ? find_rank(R, D, c) : -1;
+        if (pos >= 0) {
+            if (pos > i && pos != j) {
+                const uint32_t kp = (R[pos] & 3u) | get2(Ba, pos) << 2;
+                const uint32_t mp = star_mask(Y, kb, kp), pl = lut[mp];
+                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);   // not a plain partner of b
+                if (pos > j) {   // the event {r, a, b, R[pos]}
+                    const uint32_t ce = lut[mp | (e & 3u) << 10];
+                    acc_add(accp(g, b, ce), 1u);
+                    acc_add(accp(g, c, ce), 1u);
+                    atomicAdd(H + ce, 1u);
+                    atomicAdd(H + pl, 0xffffffffu);
                 }
-                emit4<C>(H, g, b, c, col, lane);
+            }
+            return kNone;
+        }
+        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
+        if (q >= 0) {   // "2+1" with c in L_a and a b-c edge: event
+            const uint32_t mp = p1_mask(Y, kb, La[q] & 3u);
+            const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+            acc_add(accp(g, b, ce), 1u);
+            acc_add(accp(g, c, ce), 1u);
+            acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
+            acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+            atomicAdd(H + ce, 1u);
+            atomicAdd(H + pl, 0xffffffffu);
+            return kNone;
+        }
+        return lut[Y | (kb & 3u) << 2 | (kb >> 2) << 6 | (e & 3u) << 10];   // "2+1" with c in L_b \ N(a)
+    };
+    // an entry e of b = L_a[x]'s list: "1+2" events (c in L_a after b), else a "1+1+1" set.  c = a
+    // (always in b's list) is in R: tested first, so that the one lane holding it does not send
+    // the whole warp through the binary search
+    auto bL_entry = [&](int x, uint32_t e, bool valid, uint32_t &c) -> int {
+        c = e >> 2;
+        if (!valid || c <= r || c == a || (fmay(FR, c) && find_rank(R, D, c) >= 0)) return kNone;
+        const uint32_t eb = La[x], b = eb >> 2, mb = Y | (eb & 3u) << 6;
+        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
+        if (q >= 0) {
+            if (q > x) {   // "1+2" with a b-c edge: event
+                const uint32_t mp = mb | (La[q] & 3u) << 8;
+                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                acc_add(accp(g, b, ce), 1u);
+                acc_add(accp(g, c, ce), 1u);
+                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
+                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+                atomicAdd(H + ce, 1u);
+                atomicAdd(H + pl, 0xffffffffu);
+            }
+            return kNone;
+        }
+        return lut[mb | (e & 3u) << 10];   // "1+1+1"
+    };
+    if (!(VDMC_SKIPF(g) & 2)) {
+        if (st->rok && i + 1 < D) {
+            flat_walk(st->RL, st->RS, i + 1, D, lane, [&](int j, uint32_t e, bool valid) {
+                uint32_t c;
+                const int col = bR_entry(j, e, valid, c);
+                emit4v<C>(H, g, R[j] >> 2, j, c, col, lane);
+            });
+        } else {
+            for (int j = i + 1; j < D; j++) {
+                const List bl = list_at(g, R, j, st->RL, st->RS, st->rok);
+                for (int base = 0; base < bl.len; base += 32) {
+                    const int p = base + lane;
+                    uint32_t c;
+                    const int col = bR_entry(j, p < bl.len ? bl.p[p] : 0u, p < bl.len, c);
+                    emit4<C>(H, g, R[j] >> 2, c, col, lane);
+                }
+                if (g.big) flush_hist<C>(H, g, r, a, lane);
             }
         }
-        // b's plain sets: "3" per partner key (lanes 1..15), "2+1" with c in L_a per w (lanes 17..19)
-        corr = __reduce_add_sync(kFull, corr);
-        if (lane < 16) {
-            if ((P >> lane) & 1u) {
-                uint32_t cnt = (uint32_t)N[lane] - ((uint32_t)lane == kb ? 1u : 0u);
-                if (lane < 4) cnt -= (corr >> (10u * ((uint32_t)lane - 1u))) & 0x3ffu;
-                if (cnt) acc_add(accp(g, b, lut[star_mask(Y, kb, (uint32_t)lane)]), cnt);
+        // b = R[j] (lanes): its plain "3" sets per partner key, "2+1" sets with c in L_a per w
+        for (int j = i + 1 + lane; j < D; j += 32) {
+            const uint32_t eb = R[j], b = eb >> 2;
+            const uint32_t kb = (eb & 3u) | get2(Ba, j) << 2;
+            for (uint32_t m = P; m; m &= m - 1u) {
+                const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                const uint32_t cnt = (uint32_t)N[k] - (k == kb ? 1u : 0u);
+                if (cnt) acc_add(accp(g, b, lut[star_mask(Y, kb, k)]), cnt);
             }
-        } else if (lane >= 17 && lane <= 19) {
-            const uint32_t w = (uint32_t)lane - 16u;
-            if (M[w]) acc_add(accp(g, b, lut[p1_mask(Y, kb, w)]), (uint32_t)M[w]);
+#pragma unroll
+            for (uint32_t w = 1; w <= 3; w++)
+                if (M[w]) acc_add(accp(g, b, lut[p1_mask(Y, kb, w)]), (uint32_t)M[w]);
         }
-        if (g.big) flush_hist<C>(H, g, r, a, lane);
+        // c in L_a (lanes): "2+1" plain (every b in R beyond i, per key), "1+2" plain (partners per w)
+        for (int q = lane; q < nL; q += 32) {
+            const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
+            for (uint32_t m = P; m; m &= m - 1u) {
+                const uint32_t k = (uint32_t)__ffs(m) - 1u;
+                acc_add(accp(g, c, lut[p1_mask(Y, k, w)]), (uint32_t)N[k]);
+            }
+#pragma unroll
+            for (uint32_t w2 = 1; w2 <= 3; w2++) {
+                const uint32_t cnt = (uint32_t)M[w2] - (w2 == w ? 1u : 0u);
+                if (cnt) acc_add(accp(g, c, lut[Y | w << 6 | w2 << 8]), cnt);
+            }
+        }
         __syncwarp();
     }
-    // c in L_a: "2+1" plain (every b in R beyond i, per key) and "1+2" plain (partners in L_a per w)
-    if (!(VDMC_SKIPF(g) & 2))
-        for (int base = 0; base < nL; base += 32) {
-            const int q = base + lane;
-            if (q < nL) {
-                const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
-                for (uint32_t m = P; m; m &= m - 1u) {
-                    const uint32_t k = (uint32_t)__ffs(m) - 1u;
-                    acc_add(accp(g, c, lut[p1_mask(Y, k, w)]), (uint32_t)N[k]);
+    if (!(VDMC_SKIPF(g) & 4)) {
+        if (st->lok && nL > 0) {
+            flat_walk(st->LL, st->LS, 0, nL, lane, [&](int x, uint32_t e, bool valid) {
+                uint32_t c;
+                const int col = bL_entry(x, e, valid, c);
+                emit4v<C>(H, g, La[x] >> 2, x, c, col, lane);
+            });
+        } else {
+            for (int x = 0; x < nL; x++) {
+                const List bl = list_at(g, La, x, st->LL, st->LS, st->lok);
+                for (int base = 0; base < bl.len; base += 32) {
+                    const int p = base + lane;
+                    uint32_t c;
+                    const int col = bL_entry(x, p < bl.len ? bl.p[p] : 0u, p < bl.len, c);
+                    emit4<C>(H, g, La[x] >> 2, c, col, lane);
                 }
-#pragma unroll
-                for (uint32_t w2 = 1; w2 <= 3; w2++) {
-                    const uint32_t cnt = (uint32_t)M[w2] - (w2 == w ? 1u : 0u);
-                    if (cnt) acc_add(accp(g, c, lut[Y | w << 6 | w2 << 8]), cnt);
-                }
+                if (g.big) flush_hist<C>(H, g, r, a, lane);
             }
         }
-    // b = L_a[x]: "1+1+1" sets per walked entry, "1+2" edge events
-    for (int x = 0; !(VDMC_SKIPF(g) & 4) && x < nL; x++) {
-        const uint32_t eb = La[x], b = eb >> 2, wb = eb & 3u;
-        const uint32_t mb = Y | wb << 6;
-        const List bl = list_at(g, La, x, st->LL, st->LS, st->lok);
-        for (int base = 0; base < bl.len; base += 32 * kPF) {
-            uint32_t ev[kPF];
-#pragma unroll
-            for (int u = 0; u < kPF; u++) {
-                const int p = base + 32 * u + lane;
-                ev[u] = p < bl.len ? bl.p[p] : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < kPF; u++) {
-                if (base + 32 * u >= bl.len) break;
-                const uint32_t e = ev[u];
-                int col = kNone;
-                uint32_t c = 0;
-                if (base + 32 * u + lane < bl.len) {
-                    c = e >> 2;
-                    // c = a (always in b's list) is in R: tested first, so that the one lane holding
-                    // it does not send the whole warp through the binary search
-                    if (c > r && c != a && (!fmay(FR, c) || find_rank(R, D, c) < 0)) {
-                        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
-                        if (q >= 0) {
-                            if (q > x) {   // "1+2" with a b-c edge: event
-                                const uint32_t mp = mb | (La[q] & 3u) << 8;
-                                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
-                                acc_add(accp(g, b, ce), 1u);
-                                acc_add(accp(g, c, ce), 1u);
-                                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
-                                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
-                                atomicAdd(H + ce, 1u);
-                                atomicAdd(H + pl, 0xffffffffu);
-                            }
-                        } else {
-                            col = lut[mb | (e & 3u) << 10];   // "1+1+1"
-                        }
-                    }
-                }
-                emit4<C>(H, g, b, c, col, lane);
-            }
-        }
-        if (g.big) flush_hist<C>(H, g, r, a, lane);
         __syncwarp();
     }
     // r and a: the plain pairs -- "3" per key pair, "2+1" with c in L_a per (key, w), "1+2" per w pair
