@@ -606,6 +606,42 @@ __device__ __forceinline__ void star_fast_any(const Dev &g, const uint32_t *R, S
     }
 }
 
+// one set with members r, a (histogram H), b (per lane: the owner of the walked entry) and c (lane):
+// b-side atomics merged over the lanes with the same (owner, column)
+template <int C>
+__device__ __forceinline__ void emit4v(uint32_t *H, const Dev &g, uint32_t b, int owner, uint32_t c, int col,
+                                       int lane) {
+    const bool v = col != kNone;
+    const uint32_t cc = v ? (uint32_t)col : 0u;
+    red_if(v, accp(g, c, cc), 1u);
+    const unsigned m = __match_any_sync(kFull, v ? ((uint32_t)owner << 8 | cc) : 0xffffffffu);
+    const bool lead = v && lane == __ffs(m) - 1;
+    const uint32_t cnt = __popc(m);
+    red_shared_if(lead, H + cc, cnt);
+    red_if(lead, accp(g, b, cc), cnt);
+}
+
+// Flattened walk over the staged lists q in [q0, q1) (pool entries [S[q0], S[q1]), every list
+// non-empty): 32 consecutive entries per pass whatever the list lengths, so short lists do not
+// leave lanes idle.  The owner of entry f is q0 + #{q in (q0, q1) : S[q] <= f}: per pass the
+// lanes load the next 32 list starts, and a bitmap of the starts inside (base, base + 32] gives
+// each lane its owner with one popc.  fn(owner, entry, valid) is called by every lane.
+template <typename Fn>
+__device__ __forceinline__ void flat_walk(const uint32_t *pool, const uint32_t *S, int q0, int q1, int lane, Fn fn) {
+    const int f1 = (int)S[q1];
+    int o = q0;
+    for (int base = (int)S[q0]; base < f1; base += 32) {
+        const int qb = o + 1 + lane;
+        const int d = qb < q1 ? (int)S[qb] - base : 64;   // start of list qb, relative to base
+        const unsigned B = __reduce_or_sync(kFull, d >= 1 && d <= 32 ? 1u << (d - 1) : 0u);
+        const int owner = o + __popc(B & ((1u << lane) - 1u));
+        const int f = base + lane;
+        const bool valid = f < f1;
+        fn(owner, valid ? pool[f] : 0u, valid);
+        o += __popc(B);
+    }
+}
+
 // ------------------------------------- shapes "3" and "2+1" at heavy roots, counted in closed form
 // Task (r, x = R[i]), Y = code(r, x).  The key of a position q != i is codes[q] = x_q | al_q << 2
 // with x_q = code(r, R[q]) and al_q = code(x, R[q]); N[k] = #{q > i : key k}, N[16 + k] =
@@ -1338,50 +1374,6 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
 // from the key counts N[k] (positions beyond i) and M[w] (|L_a| per code(a, c)), with their
 // edge pairs as events (classified alone, taken back from the plain counts); the sets that need
 // a walked entry -- "2+1" with c in L_b \ N(a), and "1+1+1" -- are enumerated one per lane as
-// before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back.
-// N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
-// one set with members r, a (histogram H), b (per lane: the owner of the walked entry) and c (lane):
-// b-side atomics merged over the lanes with the same (owner, column)
-template <int C>
-__device__ __forceinline__ void emit4v(uint32_t *H, const Dev &g, uint32_t b, int owner, uint32_t c, int col,
-                                       int lane) {
-    const bool v = col != kNone;
-    const uint32_t cc = v ? (uint32_t)col : 0u;
-    red_if(v, accp(g, c, cc), 1u);
-    const unsigned m = __match_any_sync(kFull, v ? ((uint32_t)owner << 8 | cc) : 0xffffffffu);
-    const bool lead = v && lane == __ffs(m) - 1;
-    const uint32_t cnt = __popc(m);
-    red_shared_if(lead, H + cc, cnt);
-    red_if(lead, accp(g, b, cc), cnt);
-}
-
-// Flattened walk over the staged lists q in [q0, q1) (pool entries [S[q0], S[q1]), every list
-// non-empty): 32 consecutive entries per pass whatever the list lengths, so short lists do not
-// leave lanes idle.  The owner of entry f is q0 + #{q in (q0, q1) : S[q] <= f}: per pass the
-// lanes load the next 32 list starts, and a bitmap of the starts inside (base, base + 32] gives
-// each lane its owner with one popc.  fn(owner, entry, valid) is called by every lane.
-template <typename Fn>
-__device__ __forceinline__ void flat_walk(const uint32_t *pool, const uint32_t *S, int q0, int q1, int lane, Fn fn) {
-    const int f1 = (int)S[q1];
-    int o = q0;
-    for (int base = (int)S[q0]; base < f1; base += 32) {
-        const int qb = o + 1 + lane;
-        const int d = qb < q1 ? (int)S[qb] - base : 64;   // start of list qb, relative to base
-        const unsigned B = __reduce_or_sync(kFull, d >= 1 && d <= 32 ? 1u << (d - 1) : 0u);
-        const int owner = o + __popc(B & ((1u << lane) - 1u));
-        const int f = base + lane;
-        const bool valid = f < f1;
-        fn(owner, valid ? pool[f] : 0u, valid);
-        o += __popc(B);
-    }
-}
-
-// ------------------------------------------------------------- light tasks (k = 4), closed form
-// One warp, the task (r, a = R[i]) of a light root, Y = code(r, a).  As at heavy roots: "3" (b, c
-// in R beyond i), "2+1" with c in L_a (every b in R beyond i) and "1+2" (b, c in L_a) are counted
-// from the key counts N[k] (positions beyond i) and M[w] (|L_a| per code(a, c)), with their
-// edge pairs as events (classified alone, taken back from the plain counts); the sets that need
-// a walked entry -- "2+1" with c in L_b \ N(a), and "1+1+1" -- are enumerated one per lane as
 // before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back; when
 // the lists are staged they are walked flattened (flat_walk), else list by list.
 // N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
@@ -1619,6 +1611,9 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         // "3" items (positions beyond i) and the "2+1" R[j]-side items (all positions), which fill
         // the warps' tails
         const int rem = D - i - 1;
+        // (measured: batching several u's per item with a flattened walk is slower, 197-277 vs 182 ms
+        // on cfg4 -- fewer items balance the warps worse and the per-entry owner shuffles cost more
+        // than the idle lanes of short lists)
         const int nu = (VDMC_SKIPF(g) & 4) ? 0 : nL;
         const int nstar = rem >= 2 ? (rem + kSPW - 1) / kSPW : 0;
         const int nj = (VDMC_SKIPF(g) & 2) || nL == 0 ? 0 : (D + kSPW - 1) / kSPW;
