@@ -824,7 +824,7 @@ void vdmc_free_graph(vdmc_graph *g) {
     cudaSetDevice(g->device);
     cudaDeviceSynchronize();
     void *ptrs[] = {g->off, g->split, g->adj, g->order, g->tfirst, g->task_root, g->lut[0][0], g->lut[0][1],
-                    g->lut[1][0], g->lut[1][1], g->heavy_task, g->light_root, g->hroots, g->hbase, g->nr_off,
+                    g->lut[1][0], g->lut[1][1], g->heavy_task, g->light_root, g->light_i0, g->hroots, g->hbase, g->nr_off,
                     g->nr_adj};
     for (void *p : ptrs) dfree(p, nullptr);
     cudaStreamSynchronize(nullptr);

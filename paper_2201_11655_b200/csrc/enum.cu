@@ -62,6 +62,8 @@ constexpr int kLightDeg = 128;        // light root: G_U degree <= this (measure
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
+constexpr int kLightChunk = 8;        // light items: at most this many tasks of one root (a root of ~100
+                                      // tasks is ~15 ms of one warp: cut, it no longer bounds a slice)
 
 // Profiling switches that DROP work (VDMC_PHASES / VDMC_SKIP / VDMC_MINREM) exist only in the
 // profiling build (-DVDMC_PROFILING, tools/build_variant.sh); the product library has none.
@@ -78,7 +80,8 @@ struct Dev {
     const int64_t *__restrict__ tfirst;
     const int32_t *__restrict__ task_root;
     const int32_t *__restrict__ heavy_task;   // task ids of heavy roots, rank order
-    const int32_t *__restrict__ light_root;   // light roots, rank order
+    const int32_t *__restrict__ light_root;   // light items (root, first task offset i0), rank order
+    const int32_t *__restrict__ light_i0;
     int64_t nheavy, nlight;
     AccT *__restrict__ acc;                   // accumulator, class-major: element (v = rank, col) at col * ns + v
     uint32_t ns;                              // column stride = n
@@ -185,16 +188,17 @@ __device__ __forceinline__ RIndex build_rindex(const uint32_t *R, int D, uint16_
     ix.lo = R[0] >> 2;
     ix.hi = R[D - 1] >> 2;
     const uint32_t span = ix.hi - ix.lo;   // buckets 0 .. span >> shift
+    const uint32_t nbmax = (uint32_t)min(kBuckets, max(32, 2 * D));   // ~2 buckets per entry: O(D) to build
     int sh = 0;
-    while ((span >> sh) >= (uint32_t)kBuckets) sh++;
+    while ((span >> sh) >= nbmax) sh++;
     ix.shift = sh;
-    const int nb = (int)(span >> sh) + 1;   // <= kBuckets
+    const int nb = (int)(span >> sh) + 1;   // <= nbmax; lookups read T[0 .. nb]
     for (int q = tid; q < D; q += nthreads) {   // T[b] = first q with bucket(R[q]) >= b
         const int bq = (int)(((R[q] >> 2) - ix.lo) >> sh);
         const int bp = q > 0 ? (int)(((R[q - 1] >> 2) - ix.lo) >> sh) : -1;
         for (int b = bp + 1; b <= bq; b++) T[b] = (uint16_t)q;
     }
-    for (int b = nb + tid; b <= kBuckets; b += nthreads) T[b] = (uint16_t)D;   // past the last bucket
+    if (tid == 0) T[nb] = (uint16_t)D;   // end of the last bucket
     ix.T = T;
     return ix;
 }
@@ -1709,9 +1713,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int64_t mid = (a + b) >> 1;   // for lo, tfirst[r] >= key for hi)
             bool before;
             if (heavy) before = g.heavy_task[mid] < key;
-            else {
+            else {   // the item's tasks [t0, t1)
                 const int64_t r = g.light_root[mid];
-                before = (tid & 1) ? g.tfirst[r] < key : g.tfirst[r + 1] <= key;
+                const int64_t t0 = g.tfirst[r] + g.light_i0[mid];
+                const int64_t t1 = min(t0 + kLightChunk, g.tfirst[r + 1]);
+                before = (tid & 1) ? t0 < key : t1 <= key;
             }
             if (before) a = mid + 1;
             else b = mid;
@@ -1817,8 +1823,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int64_t li = s_sub[2] + (int64_t)__shfl_sync(kFull, x, 0);
             if (li >= s_sub[3]) break;
             const uint32_t r = (uint32_t)g.light_root[li];
-            const int64_t t0 = g.tfirst[r], t1 = g.tfirst[r + 1];
-            const int64_t ta = max(t0, lo), tb = min(t1, hi);
+            const int64_t t0 = g.tfirst[r];   // the item's tasks: [t0 + i0, t0 + i0 + kLightChunk) of the root
+            const int64_t ti = t0 + g.light_i0[li];
+            const int64_t ta = max(ti, lo), tb = min(min(ti + kLightChunk, g.tfirst[r + 1]), hi);
             if (ta >= tb) continue;
             const int64_t rs = g.split[r];
             const int D = (int)(g.off[r + 1] - rs);
@@ -1947,10 +1954,11 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
         if (k == 3) {
             const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
             c = heavy ? 92290 + 50 * (rem + da) : 1454 + 10 * (rem + nla) + suf + s2[a] / 8;
-        } else if (heavy) {
-            c = 92290 + rem * rem * 9151 / 100000 + nla * D * 3528 / 1000;
-        } else {
-            c = 1454 + rem * nla * 1275 / 100 + nla * nla * 49;
+        } else if (heavy) {   // k = 4, closed-form heavy task: per-task overhead, O(rem) items, R staging
+            c = 20980 + rem * 5542 / 100 + (ia == rs ? D * 27350 : 0);
+        } else {              // light task: b-in-R walks (suffix of forward degrees), per-root staging
+            const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
+            c = suf * 4547 / 100 + (ia == rs ? 3757 : 0);
         }
         cost[t] = c;
     }
@@ -2017,6 +2025,24 @@ __global__ void __launch_bounds__(512) k_nr(const int64_t *__restrict__ off, con
         }
         __syncthreads();
     }
+}
+
+__global__ void k_light_parts(int64_t nl, const int32_t *__restrict__ lroots, const int64_t *__restrict__ tfirst,
+                              int64_t *__restrict__ cnt) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nl; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = lroots[q], nt = tfirst[r + 1] - tfirst[r];
+        cnt[q] = (nt + kLightChunk - 1) / kLightChunk;
+    }
+}
+
+__global__ void k_light_scatter(int64_t nl, const int32_t *__restrict__ lroots, const int64_t *__restrict__ cnt,
+                                const int64_t *__restrict__ base, int32_t *__restrict__ iroot,
+                                int32_t *__restrict__ i0) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nl; q += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t p = 0; p < cnt[q]; p++) {
+            iroot[base[q] + p] = lroots[q];
+            i0[base[q] + p] = (int32_t)(p * kLightChunk);
+        }
 }
 
 __global__ void k_heavy_d(int64_t nh, const int32_t *__restrict__ hroots, const int64_t *__restrict__ off,
@@ -2115,6 +2141,35 @@ vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s) {
     g->nheavy = hn[0];
     g->nlight = hn[1];
     g->nhroots = nhr;
+    if (g->nlight > 0) {   // light items: each light root's tasks in chunks of <= kLightChunk
+        const int64_t nl = g->nlight;
+        int64_t *cnt = nullptr, *base = nullptr;
+        VDMC_CUDA(dalloc((void **)&cnt, sizeof(int64_t) * (nl + 1), s));
+        VDMC_CUDA(dalloc((void **)&base, sizeof(int64_t) * (nl + 1), s));
+        VDMC_CUDA(cudaMemsetAsync(cnt + nl, 0, sizeof(int64_t), s));
+        k_light_parts<<<148 * 4, 256, 0, s>>>(nl, g->light_root, g->tfirst, cnt);
+        VDMC_LAUNCH();
+        size_t tb = 0;
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, base, (int)(nl + 1), s));
+        void *ts = nullptr;
+        VDMC_CUDA(dalloc((void **)&ts, tb, s));
+        VDMC_CUDA(cub::DeviceScan::ExclusiveSum(ts, tb, cnt, base, (int)(nl + 1), s));
+        count_launch(1);
+        int64_t nitems = 0;
+        VDMC_CUDA(cudaMemcpyAsync(&nitems, base + nl, sizeof nitems, cudaMemcpyDeviceToHost, s));
+        VDMC_CUDA(cudaStreamSynchronize(s));
+        int32_t *iroot = nullptr;
+        VDMC_CUDA(dalloc((void **)&iroot, sizeof(int32_t) * nitems, s));
+        VDMC_CUDA(dalloc((void **)&g->light_i0, sizeof(int32_t) * nitems, s));
+        k_light_scatter<<<148 * 4, 256, 0, s>>>(nl, g->light_root, cnt, base, iroot, g->light_i0);
+        VDMC_LAUNCH();
+        dfree(g->light_root, s);
+        g->light_root = iroot;
+        g->nlight = nitems;
+        dfree(ts, s);
+        dfree(cnt, s);
+        dfree(base, s);
+    }
     if (nhr > 0) {
         int64_t *dlist = nullptr, *segs = nullptr;
         VDMC_CUDA(dalloc((void **)&dlist, sizeof(int64_t) * (nhr + 1), s));
@@ -2258,6 +2313,7 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     d.task_root = g->task_root;
     d.heavy_task = g->heavy_task;
     d.light_root = g->light_root;
+    d.light_i0 = g->light_i0;
     d.nheavy = g->nheavy;
     d.nlight = g->nlight;
 #ifdef VDMC_PROFILING

@@ -80,7 +80,8 @@ struct vdmc_graph {
     // S4 schedule: tasks of heavy roots (CTA per task) and light roots (warp per root), both
     // ascending (= rank order, longest first), so a task slice maps to a contiguous sub-list
     int32_t *heavy_task = nullptr; // [nheavy]
-    int32_t *light_root = nullptr; // [nlight]
+    int32_t *light_root = nullptr; // [nlight] light items: root, and the item's first task offset in
+    int32_t *light_i0 = nullptr;   // [nlight] the root (a root of D tasks is cut into items of <= 8 tasks)
     int64_t nheavy = 0, nlight = 0;
     // induced adjacency of N+(r) in position space for heavy roots r (S4 pre-pass):
     // entries of the position p of root r: nr_adj[nr_off[hbase[r] + p] .. nr_off[hbase[r] + p + 1])
