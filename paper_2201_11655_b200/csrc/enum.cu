@@ -1954,11 +1954,12 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
         if (k == 3) {
             const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
             c = heavy ? 92290 + 50 * (rem + da) : 1454 + 10 * (rem + nla) + suf + s2[a] / 8;
-        } else if (heavy) {   // k = 4, closed-form heavy task: per-task overhead, O(rem) items, R staging
-            c = 20980 + rem * 5542 / 100 + (ia == rs ? D * 27350 : 0);
-        } else {              // light task: b-in-R walks (suffix of forward degrees), per-root staging
+        } else if (heavy) {   // k = 4 closed-form heavy task (units of 1e-9 ms; tools/fit_plan.py, profiles/r02_planner_fit.txt):
+                              // per-task overhead (barriers, phase A), O(D) items, walks of L_a
+            c = 21090 + D * 2452 / 100 + nla * 871;
+        } else {              // light task: b-in-R walks (suffix of forward degrees), L_a walks, per-root staging
             const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
-            c = suf * 4547 / 100 + (ia == rs ? 3757 : 0);
+            c = suf * 3614 / 100 + nla * 104 + (ia == rs ? 3898 : 0);
         }
         cost[t] = c;
     }
