@@ -338,6 +338,7 @@ def main():
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         build_ms = g.info["build_ms"]
+        maxdeg = g.info["max_degree"]
         if tm:
             enum_ms.append(tm["enum"])
             phase_ms.append({"build": build_ms, **tm})
@@ -396,6 +397,10 @@ def main():
         e2e_motifs = motifs_of(h_out)
         assert e2e_motifs == motifs[0], "e2e result differs from the device-resident steps"
 
+    # accumulator word of the count (the library's rule, vdmc.h acc64): 32-bit when no (vertex,
+    # class) count can reach 2^32 -- 6 maxdeg^3 (k = 4) / 2 maxdeg^2 (k = 3); the output is u64
+    acc_dtype = "u32" if (6 * maxdeg ** 3 if k == 4 else 2 * maxdeg ** 2) < 2 ** 32 and k in (3, 4) \
+        and not args.edges else "u64"
     if rank == 0:
         assert len(set(motifs)) == 1, f"motif totals differ between steps: {motifs}"
         total_sets = motifs[0]
@@ -405,7 +410,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "motifs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "vs_baseline": None, "dtype": acc_dtype, "data": "synthetic",
             "edges_per_sec": arcs / (ms_per_step / 1e3),
             "motifs_per_step": total_sets,
             "step_ms": {"mean": ms_per_step, "median": statistics.median(step_ms), "best": min(step_ms),
@@ -429,7 +434,8 @@ def main():
                                  "enum_share": enum_avg / ms_per_step,
                                  **{f"{key}_avg": statistics.mean(t[key] for t in phase_ms)
                                     for key in ("build", "schedule", "finalize")}}
-            line["roofline"] = roofline(args, k, total_sets, enum_avg, peak, peak_src)
+            line["roofline"] = roofline(args, k, total_sets, enum_avg, peak, peak_src,
+                                        float((clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0))
             if args.edges:
                 line["roofline"]["kernel"] = f"k_edges<{k}>"
         if world == 1 and not args.no_cpu_baseline:
@@ -444,31 +450,37 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(args, k, motifs, enum_ms, peak, peak_src):
-    """SURVEY §8(d) roofline of the dominant kernel (k_enum), per launch (N = 1).
-    frac     : M3 model, algorithmic bytes = motifs x B_k,eff over the live kernel time, vs the
-               measured HBM copy bandwidth.  B_k,eff = 4 + 16 x (L2 atomic/reduction requests per
-               motif) from ncu on this workload.
-    dram_frac: measured DRAM bytes per launch (ncu) over the live kernel time, vs the same peak.
-    issue_frac: warp instructions issued / (SMSPs x cycles) in the ncu capture."""
+def roofline(args, k, motifs, enum_ms, peak, peak_src, sm_mhz):
+    """Roofline of the dominant kernel (k_enum), per launch (N = 1); DESIGN.md §4 "Roofline".
+    The path is integer and irregular, and its closed forms count most sets without touching
+    them, so no per-motif byte count bounds it.  Headline ("alu"): the instruction issue of the
+    SMs -- achieved = warp instructions per launch (ncu smsp__inst_executed.sum, committed under
+    profiles/) over the live kernel time; peak = 148 SMs x 4 schedulers x 1 warp instruction per
+    clock at the measured SM clock (B300_MICROARCH.md / B200_PROFILING.md unit counts).
+    Reported beside it: hbm = measured DRAM bytes per launch (ncu) over the live time vs the
+    measured HBM copy bandwidth, and the SURVEY §8(d) M3 per-motif model (4 B + 16 B per atomic
+    reaching L2, per motif), which the closed forms undercut (frac > 1: not a bound)."""
     t = enum_ms / 1e3
     c = ncu_counters(args.config + ("-edges" if args.edges else ""), k, args.kind)
-    roof = {"bound": "hbm", "kernel": f"k_enum<{k}>", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+    peak_issue = 148 * 4 * sm_mhz / 1e3   # G warp-instructions / s
+    roof = {"bound": "alu", "kernel": f"k_enum<{k}>", "unit": "Gwarp-inst/s", "peak": peak_issue,
+            "peak_source": f"148 SMs x 4 schedulers x 1 warp-instruction/clock x {sm_mhz:.0f} MHz (measured SM clock)",
             "motifs_per_launch": motifs}
-    b_full = 4 + 16 * (k - 1)
-    roof["B_k"] = b_full
-    roof["frac_B_k"] = motifs * b_full / t / 1e9 / peak
-    if c and "l2_red_requests" in c:
+    if c and "warp_insts" in c:
+        achieved = c["warp_insts"] / t / 1e9
         atoms = c["l2_red_requests"] + c.get("l2_atom_requests", 0)
         b_eff = 4 + 16 * atoms / motifs
-        achieved = motifs * b_eff / t / 1e9
-        roof.update({"achieved": achieved, "frac": achieved / peak, "B_k_eff": b_eff,
-                     "atomics_per_motif": atoms / motifs, "traffic": c["dram_bytes"],
-                     "dram_GBs": c["dram_bytes"] / t / 1e9, "dram_frac": c["dram_bytes"] / t / 1e9 / peak,
-                     "issue_frac": c.get("issue_frac"), "l2_hit_pct": c.get("l2_hit_pct"),
-                     "l2_red_hit_pct": c.get("l2_red_hit_pct"), "warps_active_pct": c.get("warps_active_pct"),
-                     "ncu_source": c.get("report"),
-                     "algorithmic": f"motifs x B_k,eff = {motifs:.4g} x {b_eff:.2f} B (SURVEY 8(d) M3)"})
+        dram = c["dram_bytes"] / t / 1e9
+        roof.update({"achieved": achieved, "frac": achieved / peak_issue, "traffic": c["dram_bytes"],
+                     "warp_insts_per_launch": c["warp_insts"],
+                     "hbm": {"achieved": dram, "peak": peak, "unit": "GB/s", "frac": dram / peak,
+                             "peak_source": peak_src},
+                     "m3_model": {"B_k_eff": b_eff, "atomics_per_motif": atoms / motifs,
+                                  "achieved": motifs * b_eff / t / 1e9, "frac": motifs * b_eff / t / 1e9 / peak,
+                                  "note": "per-motif model of SURVEY 8(d) M3; the closed forms count most "
+                                          "sets without a per-set read or atomic, so it does not bound k_enum"},
+                     "l2_hit_pct": c.get("l2_hit_pct"), "l2_red_hit_pct": c.get("l2_red_hit_pct"),
+                     "warps_active_pct": c.get("warps_active_pct"), "ncu_source": c.get("report")})
     else:
         roof.update({"achieved": None, "frac": None, "traffic": None,
                      "note": "no ncu counters committed for this workload (profiles/ncu_traffic.json)"})

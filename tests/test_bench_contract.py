@@ -54,7 +54,9 @@ def test_bench_line_gpu_small():
         assert key in line, key
     assert line["n_gpus"] == 1 and line["steps"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     roof = line["roofline"]
-    assert roof["bound"] == "hbm" and roof["frac_B_k"] > 0
-    assert roof["frac"] is None or 0 < roof["frac"] < 1.2
+    assert roof["bound"] == "alu" and roof["peak"] > 0 and roof["unit"] == "Gwarp-inst/s"
+    assert roof["frac"] is None or 0 < roof["frac"] <= 1.0
+    assert roof["frac"] is None or 0 < roof["hbm"]["frac"] <= 1.0
+    assert line["dtype"] in ("u32", "u64")
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert "workload" in line["config"]
