@@ -62,6 +62,7 @@ constexpr int kLightDeg = 128;        // light root: G_U degree <= this (measure
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
+constexpr int kHChunk = 8;            // heavy tasks fetched per CTA request
 constexpr int kLightChunk = 8;        // light items: at most this many tasks of one root (a root of ~100
                                       // tasks is ~15 ms of one warp: cut, it no longer bounds a slice)
 
@@ -1738,13 +1739,18 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         __syncthreads();
         int64_t staged = -1;
         RIndex rix{0u, 0u, 0, nullptr};
+        int64_t h = 0, hend = 0;
         for (;;) {   // bounds re-read from shared memory (keeps them out of the loop's registers)
-            if (tid == 0) s_item = s_sub[0] + (int64_t)atomicAdd(ctr, 1ull);
-            __syncthreads();
-            const int64_t h = s_item;
-            __syncthreads();
+            if (h >= hend) {   // kHChunk consecutive tasks per fetch: one R staging for a small root's
+                               // tasks, and two barriers per chunk instead of per task
+                if (tid == 0) s_item = s_sub[0] + (int64_t)atomicAdd(ctr, (unsigned long long)kHChunk);
+                __syncthreads();
+                h = s_item;
+                hend = h + kHChunk;
+                __syncthreads();
+            }
             if (h >= s_sub[1]) break;
-            const int64_t t = g.heavy_task[h];
+            const int64_t t = g.heavy_task[h++];
             const uint32_t r = (uint32_t)g.task_root[t];
             const int64_t rs = g.split[r];
             const int D = (int)(g.off[r + 1] - rs);
