@@ -330,19 +330,23 @@ __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S
     if (lane == 0) S[m] = (uint32_t)total;
     __syncwarp();
     // asynchronous global -> shared copies (cp.async): every entry of the gather is in flight at
-    // once instead of one dependent load per lane and step
-#pragma unroll 4
-    for (int f = lane; f < total; f += 32) {
-        int lo = 0, hi = m;   // last q with S[q] <= f
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if ((int)S[mid] <= f) lo = mid;
-            else hi = mid;
+    // once instead of one dependent load per lane and step.  The list holding entry f: as in
+    // flat_walk, 32 consecutive entries per pass, a bitmap of the list starts inside (base,
+    // base + 32] and one popc (every staged list is non-empty: its vertex is adjacent to r or a)
+    int o = 0;
+    for (int base = 0; base < total; base += 32) {
+        const int qb = o + 1 + lane;
+        const int d = qb < m ? (int)S[qb] - base : 64;
+        const unsigned E = __reduce_or_sync(kFull, d >= 1 && d <= 32 ? 1u << (d - 1) : 0u);
+        const int own = o + __popc(E & ((1u << lane) - 1u));
+        o += __popc(E);
+        const int f = base + lane;
+        if (f < total) {
+            const uint32_t *src = g.adj + ((int64_t)O[own] + (f - (int)S[own]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(B + f)),
+                         "l"(src)
+                         : "memory");
         }
-        const uint32_t *src = g.adj + ((int64_t)O[lo] + (f - (int)S[lo]));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((uint32_t)__cvta_generic_to_shared(B + f)),
-                     "l"(src)
-                     : "memory");
     }
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
