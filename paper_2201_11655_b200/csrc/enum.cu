@@ -296,8 +296,12 @@ __device__ __forceinline__ List glist(const Dev &g, uint32_t v) {
 // q's list, S[m] = total, O[q] = its global offset.  One flattened pass, every load
 // independent (memory-level parallelism instead of one dependent chain per list).
 // Returns false (and stages nothing) if m > smax or the lists exceed cap.  One warp.
+__device__ __forceinline__ void gather_wait() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+}
 __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S, uint32_t *O, int smax, uint32_t *B,
-                             int cap, int lane) {
+                             int cap, int lane, bool wait = true) {
     if (m > smax) return false;
     int total = 0;
     for (int b0 = 0; b0 < m; b0 += 32) {
@@ -348,8 +352,8 @@ __device__ bool gather_lists(const Dev &g, const uint32_t *V, int m, uint32_t *S
                          : "memory");
         }
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    __syncwarp();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if (wait) gather_wait();   // else the caller waits (gather_wait) before reading B
     return true;
 }
 
@@ -1516,6 +1520,7 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
         }
         __syncwarp();
     }
+    if (st->lok) gather_wait();   // the L_a lists' copies (issued before the filter build)
     if (!(VDMC_SKIPF(g) & 4)) {
         if (st->lok && nL > 0) {
             flat_walk(st->LL, st->LS, 0, nL, lane, [&](int x, uint32_t e, bool valid) {
@@ -1863,11 +1868,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                     __syncwarp();
                 }
                 const int nL = build_a(r, al, R, D, Ba, La, lane, FR);
+                // closed form: the L_a lists' copies stay in flight through the filter build and the b
+                // walks over R; light_task_closed waits for them before the walks over L_a
+                const bool closed = K == 4 && g.fold <= 0;
+                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane, !closed);
                 FL[lane] = 0;
                 __syncwarp();
                 for (int q = lane; q < nL; q += 32) fadd(FL, La[q] >> 2);
                 __syncwarp();
-                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane);
                 if (K == 4 && g.fold <= 0)
                     light_task_closed<C>(g, lut, r, i, R, D, Ba, La, nL, H, reinterpret_cast<int *>(Bb),
                                          reinterpret_cast<int *>(FL + kFW), &st, lane);
