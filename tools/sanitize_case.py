@@ -22,7 +22,8 @@ for k in (3, 4):
     for kind in ("directed", "undirected"):
         out = gr.count(k, kind=kind)
         tot[(k, kind)] = int(out.sum().item())
-opts = [{"heavy_global": 1}, {"ca_capacity": 3, "star_block": 7, "cross_block": 32, "force_big": 1}]
+opts = [{"heavy_global": 1}, {"heavy_global": 1, "force_big": 1}, {"star_block": 1023},
+        {"ca_capacity": 3, "star_block": 7, "cross_block": 32, "force_big": 1}]   # closed forms + enumerated path
 for o in opts:
     assert int(gr.count(4, options=o).sum().item()) == tot[(4, "directed")], o
 acc = None
