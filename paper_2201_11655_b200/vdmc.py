@@ -210,7 +210,10 @@ class Graph:
         if rank is not None:
             rk = np.ascontiguousarray(rank, dtype=np.int32)
         if isinstance(src, torch.Tensor) and src.is_cuda:
-            assert src.dtype == torch.int32 and dst.dtype == torch.int32
+            if not (isinstance(dst, torch.Tensor) and dst.is_cuda and dst.device == src.device):
+                raise ValueError("src and dst must be CUDA tensors on the same device")
+            if src.dtype != torch.int32 or dst.dtype != torch.int32 or src.numel() != dst.numel():
+                raise ValueError("src and dst must be int32 tensors of equal length")
             src, dst = src.contiguous(), dst.contiguous()
             device = src.device.index
             with torch.cuda.device(device):
