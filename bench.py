@@ -466,7 +466,8 @@ def roofline(args, k, motifs, enum_ms, peak, peak_src, sm_mhz):
     roof = {"bound": "alu", "kernel": f"k_enum<{k}>", "unit": "Gwarp-inst/s", "peak": peak_issue,
             "peak_source": f"148 SMs x 4 schedulers x 1 warp-instruction/clock x {sm_mhz:.0f} MHz (measured SM clock)",
             "motifs_per_launch": motifs}
-    if c and "warp_insts" in c:
+    stale = bool(c) and abs(c.get("duration_ms", 0.0) - enum_ms) > 0.15 * enum_ms
+    if c and "warp_insts" in c and not stale:
         achieved = c["warp_insts"] / t / 1e9
         atoms = c["l2_red_requests"] + c.get("l2_atom_requests", 0)
         b_eff = 4 + 16 * atoms / motifs
@@ -480,7 +481,12 @@ def roofline(args, k, motifs, enum_ms, peak, peak_src, sm_mhz):
                                   "note": "per-motif model of SURVEY 8(d) M3; the closed forms count most "
                                           "sets without a per-set read or atomic, so it does not bound k_enum"},
                      "l2_hit_pct": c.get("l2_hit_pct"), "l2_red_hit_pct": c.get("l2_red_hit_pct"),
-                     "warps_active_pct": c.get("warps_active_pct"), "ncu_source": c.get("report")})
+                     "warps_active_pct": c.get("warps_active_pct"), "ncu_source": c.get("report"),
+                     "ncu_duration_ms": c.get("duration_ms")})
+    elif stale:   # counters of another build of the kernel: their instruction count does not describe this one
+        roof.update({"achieved": None, "frac": None, "traffic": None,
+                     "note": f"committed ncu counters ({c.get('report')}, {c.get('duration_ms'):.1f} ms) are from "
+                             f"another build of the kernel (live {enum_ms:.1f} ms): re-capture"})
     else:
         roof.update({"achieved": None, "frac": None, "traffic": None,
                      "note": "no ncu counters committed for this workload (profiles/ncu_traffic.json)"})

@@ -19,6 +19,3 @@ for c in cfg4 cfg5; do
   python tools/ncu_summary.py $O/enum_$c.ncu-rep "$c k=4 k_enum" > $O/enum_${c}_summary.txt 2>&1
 done
 timeout 3000 python -m pytest tests -m gpu -q -rf --durations=15 > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-timeout 1500 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_case.py > $O/memcheck.txt 2>&1; echo "rc=$?" >> $O/memcheck.txt
-timeout 1500 compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_case.py quick > $O/racecheck.txt 2>&1; echo "rc=$?" >> $O/racecheck.txt
-timeout 1500 compute-sanitizer --tool synccheck --print-limit 50 python tools/sanitize_case.py quick > $O/synccheck.txt 2>&1; echo "rc=$?" >> $O/synccheck.txt
