@@ -438,6 +438,8 @@ def main():
                                         float((clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0))
             if args.edges:
                 line["roofline"]["kernel"] = f"k_edges<{k}>"
+            elif k == 5:
+                line["roofline"]["kernel"] = "k_layers<5>"
         if world == 1 and not args.no_cpu_baseline:
             rate, sets, dt, hi, cores = oracle_sample((n, src, dst), k, args.cpu_seconds)
             line["cpu_baseline"] = {"value": rate, "unit": "motifs/s", "cores": cores, "kind": "oracle",

@@ -107,6 +107,8 @@ struct Dev {
     const int64_t *__restrict__ hbase;        // heavy root -> segment of nr_off
     const int64_t *__restrict__ nr_off;       // induced adjacency of N+(r), position space
     const uint32_t *__restrict__ nr_adj;
+    uint32_t *__restrict__ gM;                // closed forms, heavy tasks: M[w] per task at (hbase[r] + i) * 4 + w;
+                                              // the "2+1" R[j] side is then added per root by k_rside
 };
 
 // shared-memory layout (words), computed on the host
@@ -124,6 +126,7 @@ constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
 constexpr int kSmax = 64;                    // light: lists staged for at most this many vertices
 constexpr int kPool = 896;                   // light: staged list entries, R's lists then L_a's lists
 constexpr int kFW = 32;                      // light: 1024-bit membership filters of R and of L_a
+constexpr int kRecCap = 128;                 // light: induced-edge records of N+(r) per item (top of the pool)
 constexpr int kLightWords = 2 * kLW + 3 * kLB + 2 * (2 * kSmax + 1) + kPool + 2 * kFW + 4;   // + M[4] (closed form)
 
 // accumulator element (v, col) at col * n + v.  Class-major: the updates of one class from many
@@ -1390,20 +1393,32 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
 // before.  The walks of b's list (b in R beyond i, b in L_a) find every event and take-back; when
 // the lists are staged they are walked flattened (flat_walk), else list by list.
 // N is the warp's 16 words at Bb (unused by this path), M its 4 words after the filters.
+// Light k = 4 task (r, x = R[i]) in closed form with the heavy partition of "2+1" (PART 1 / PART 2,
+// as at heavy roots): no walk of R's lists per task.  A light root's tasks all take this path, so
+// every "2+1" set {r, a < b, c} is counted once, in the task of the first depth-1 vertex c hangs
+// off.  Per task: the key counts N (beyond i: slots 0..15, before i: 16..31) and M;
+// the "3" take-backs and events from the item's induced-edge records (rec[0..nrec): q | p << 8 |
+// code(R[q], R[p]) << 16, both directions, every position > the item's first task; when they did
+// not fit, rec == nullptr and R's lists beyond i are walked for their R entries instead); the
+// R[j] side of "3" (j > i) and "2+1" (all j != i); the c side of "2+1" / "1+2" for c in L_x; one
+// walk per u in L_x (part-1 events and part-2 removals for u ~ R[j], "1+2" events, "1+1+1"
+// sets); the plain pairs of r and x.  N: 32 ints, M: 4 ints of the warp's scratch.
 template <int C>
-__device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *lut, uint32_t r, int i,
-                                                  const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La,
-                                                  int nL, uint32_t *H, int *N, int *M, const Staged *st, int lane) {
-    const uint32_t Y = R[i] & 3u, a = R[i] >> 2;
+__device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, uint32_t r, int i,
+                                              const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La,
+                                              int nL, uint32_t *H, int *N, int *M, const Staged *st,
+                                              const uint32_t *rec, int nrec, int lane) {
+    const uint32_t Y = R[i] & 3u, x = R[i] >> 2;
     const uint32_t *FR = st->FR, *FL = st->FL;
-    if (lane < 16) N[lane] = 0;
+    auto key = [&](int q) -> uint32_t { return (R[q] & 3u) | get2(Ba, q) << 2; };
+    N[lane] = 0;
     if (lane < 4) M[lane] = 0;
     __syncwarp();
-    for (int base = i + 1; base < D; base += 32) {   // one leader per distinct key: no race
+    for (int base = 0; base < D; base += 32) {   // one leader per distinct slot: no race
         const int q = base + lane;
-        const uint32_t key = q < D ? (R[q] & 3u) | get2(Ba, q) << 2 : 0u;
-        const unsigned m = __match_any_sync(kFull, key);
-        if (key && lane == __ffs(m) - 1) N[key] += __popc(m);
+        const uint32_t slot = q < D && q != i ? key(q) | (q < i ? 16u : 0u) : 0u;
+        const unsigned m = __match_any_sync(kFull, slot);
+        if (slot && lane == __ffs(m) - 1) N[slot] += __popc(m);
     }
     for (int base = 0; base < nL; base += 32) {
         const int q = base + lane;
@@ -1412,138 +1427,135 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
         if (w && lane == __ffs(m) - 1) M[w] += __popc(m);
     }
     __syncwarp();
-    const uint32_t P = __ballot_sync(kFull, lane < 16 && N[lane] > 0);   // keys present beyond i
-    // an entry e of b = R[j]'s list (j > i): induced edges of the "3" sets (take-back, event if
-    // beyond b), "2+1" events (c in L_a adjacent to b), else a "2+1" set with c in L_b \ N(a)
-    auto bR_entry = [&](int j, uint32_t e, bool valid, uint32_t &c) -> int {
-        c = e >> 2;
-        if (!valid || c <= r) return kNone;
-        const uint32_t eb = R[j], b = eb >> 2;
-        const uint32_t kb = (eb & 3u) | get2(Ba, j) << 2;
-        const int pos = fmay(FR, c) ? find_rank(R, D, c) : -1;
-        if (pos >= 0) {
-            if (pos > i && pos != j) {
-                const uint32_t kp = (R[pos] & 3u) | get2(Ba, pos) << 2;
-                const uint32_t mp = star_mask(Y, kb, kp), pl = lut[mp];
-                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);   // not a plain partner of b
-                if (pos > j) {   // the event {r, a, b, R[pos]}
-                    const uint32_t ce = lut[mp | (e & 3u) << 10];
-                    acc_add(accp(g, b, ce), 1u);
-                    acc_add(accp(g, c, ce), 1u);
-                    atomicAdd(H + ce, 1u);
-                    atomicAdd(H + pl, 0xffffffffu);
-                }
-            }
-            return kNone;
-        }
-        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
-        if (q >= 0) {   // "2+1" with c in L_a and a b-c edge: event
-            const uint32_t mp = p1_mask(Y, kb, La[q] & 3u);
-            const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
-            acc_add(accp(g, b, ce), 1u);
-            acc_add(accp(g, c, ce), 1u);
-            acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
-            acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
+    const uint32_t PP = __ballot_sync(kFull, N[lane] > 0);   // slots present (beyond | before << 16)
+    const uint32_t P = PP & 0xffffu;
+    // "3": an induced edge R[q] - R[p] (q, p > i) is not a plain partner of R[q]; q < p: the event
+    // {r, x, R[q], R[p]}, classified by its full mask
+    auto rec_act = [&](int q, int p, uint32_t z) {
+        const uint32_t kq = key(q), kp = key(p);
+        const uint32_t mp = star_mask(Y, kq, kp), pl = lut[mp];
+        acc_addw(accp(g, R[q] >> 2, pl), (AccT)0 - (AccT)1);
+        if (p > q) {
+            const uint32_t ce = lut[mp | z << 10];
+            acc_add(accp(g, R[q] >> 2, ce), 1u);
+            acc_add(accp(g, R[p] >> 2, ce), 1u);
             atomicAdd(H + ce, 1u);
             atomicAdd(H + pl, 0xffffffffu);
-            return kNone;
         }
-        return lut[Y | (kb & 3u) << 2 | (kb >> 2) << 6 | (e & 3u) << 10];   // "2+1" with c in L_b \ N(a)
     };
-    // an entry e of b = L_a[x]'s list: "1+2" events (c in L_a after b), else a "1+1+1" set.  c = a
-    // (always in b's list) is in R: tested first, so that the one lane holding it does not send
-    // the whole warp through the binary search
-    auto bL_entry = [&](int x, uint32_t e, bool valid, uint32_t &c) -> int {
-        c = e >> 2;
-        if (!valid || c <= r || c == a || (fmay(FR, c) && find_rank(R, D, c) >= 0)) return kNone;
-        const uint32_t eb = La[x], b = eb >> 2, mb = Y | (eb & 3u) << 6;
-        const int q = fmay(FL, c) ? find_rank(La, nL, c) : -1;
-        if (q >= 0) {
-            if (q > x) {   // "1+2" with a b-c edge: event
-                const uint32_t mp = mb | (La[q] & 3u) << 8;
-                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
-                acc_add(accp(g, b, ce), 1u);
-                acc_add(accp(g, c, ce), 1u);
-                acc_addw(accp(g, b, pl), (AccT)0 - (AccT)1);
-                acc_addw(accp(g, c, pl), (AccT)0 - (AccT)1);
-                atomicAdd(H + ce, 1u);
-                atomicAdd(H + pl, 0xffffffffu);
-            }
-            return kNone;
+    if (rec) {
+        for (int t = lane; t < nrec; t += 32) {
+            const uint32_t v = rec[-1 - t];
+            const int q = (int)(v & 0xffu), p = (int)((v >> 8) & 0xffu);
+            if (q > i && p > i) rec_act(q, p, v >> 16);
         }
-        return lut[mb | (e & 3u) << 10];   // "1+1+1"
-    };
-    if (!(VDMC_SKIPF(g) & 2)) {
-        if (st->rok && i + 1 < D) {
-            flat_walk(st->RL, st->RS, i + 1, D, lane, [&](int j, uint32_t e, bool valid) {
-                uint32_t c;
-                const int col = bR_entry(j, e, valid, c);
-                emit4v<C>(H, g, R[j] >> 2, j, c, col, lane);
-            });
-        } else {
-            for (int j = i + 1; j < D; j++) {
-                const List bl = list_at(g, R, j, st->RL, st->RS, st->rok);
-                for (int base = 0; base < bl.len; base += 32) {
-                    const int p = base + lane;
-                    uint32_t c;
-                    const int col = bR_entry(j, p < bl.len ? bl.p[p] : 0u, p < bl.len, c);
-                    emit4<C>(H, g, R[j] >> 2, c, col, lane);
-                }
-                if (g.big) flush_hist<C>(H, g, r, a, lane);
+    } else if (i + 1 < D) {
+        const uint32_t xi = x;
+        auto ent = [&](int q, uint32_t e, bool valid) {
+            const uint32_t c = e >> 2;
+            if (valid && c > xi && fmay(FR, c)) {
+                const int p = find_rank(R, D, c);
+                if (p >= 0) rec_act(q, p, e & 3u);
             }
-        }
-        // b = R[j] (lanes): its plain "3" sets per partner key, "2+1" sets with c in L_a per w
-        for (int j = i + 1 + lane; j < D; j += 32) {
-            const uint32_t eb = R[j], b = eb >> 2;
-            const uint32_t kb = (eb & 3u) | get2(Ba, j) << 2;
+        };
+        if (st->rok) flat_walk(st->RL, st->RS, i + 1, D, lane, ent);
+        else
+            for (int q = i + 1; q < D; q++) {
+                const List bl = glist(g, R[q] >> 2);
+                for (int p = lane; p < bl.len; p += 32) ent(q, bl.p[p], true);
+            }
+    }
+    // R[j] (lanes): plain "3" sets per partner key (j > i), plain "2+1" sets per w (part 1 / 2)
+    for (int j = lane; j < D; j += 32) {
+        if (j == i) continue;
+        const uint32_t b = R[j] >> 2, kb = key(j);
+        if (j > i)
             for (uint32_t m = P; m; m &= m - 1u) {
                 const uint32_t k = (uint32_t)__ffs(m) - 1u;
                 const uint32_t cnt = (uint32_t)N[k] - (k == kb ? 1u : 0u);
                 if (cnt) acc_add(accp(g, b, lut[star_mask(Y, kb, k)]), cnt);
             }
 #pragma unroll
-            for (uint32_t w = 1; w <= 3; w++)
-                if (M[w]) acc_add(accp(g, b, lut[p1_mask(Y, kb, w)]), (uint32_t)M[w]);
+        for (uint32_t w = 1; w <= 3; w++)
+            if (M[w]) acc_add(accp(g, b, lut[j > i ? p1_mask(Y, kb, w) : p2_mask(Y, kb, w)]), (uint32_t)M[w]);
+    }
+    // c in L_x (lanes): plain "2+1" sets per (part, key), plain "1+2" sets per partner code
+    for (int q = lane; q < nL; q += 32) {
+        const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
+        for (uint32_t m = PP; m; m &= m - 1u) {
+            const uint32_t s = (uint32_t)__ffs(m) - 1u, k = s & 15u;
+            acc_add(accp(g, c, lut[s < 16 ? p1_mask(Y, k, w) : p2_mask(Y, k, w)]), (uint32_t)N[s]);
         }
-        // c in L_a (lanes): "2+1" plain (every b in R beyond i, per key), "1+2" plain (partners per w)
-        for (int q = lane; q < nL; q += 32) {
-            const uint32_t ec = La[q], c = ec >> 2, w = ec & 3u;
-            for (uint32_t m = P; m; m &= m - 1u) {
-                const uint32_t k = (uint32_t)__ffs(m) - 1u;
-                acc_add(accp(g, c, lut[p1_mask(Y, k, w)]), (uint32_t)N[k]);
-            }
 #pragma unroll
-            for (uint32_t w2 = 1; w2 <= 3; w2++) {
-                const uint32_t cnt = (uint32_t)M[w2] - (w2 == w ? 1u : 0u);
-                if (cnt) acc_add(accp(g, c, lut[Y | w << 6 | w2 << 8]), cnt);
-            }
+        for (uint32_t w2 = 1; w2 <= 3; w2++) {
+            const uint32_t cnt = (uint32_t)M[w2] - (w2 == w ? 1u : 0u);
+            if (cnt) acc_add(accp(g, c, lut[Y | w << 6 | w2 << 8]), cnt);
         }
-        __syncwarp();
     }
-    if (st->lok) gather_wait();   // the L_a lists' copies (issued before the filter build)
-    if (!(VDMC_SKIPF(g) & 4)) {
-        if (st->lok && nL > 0) {
-            flat_walk(st->LL, st->LS, 0, nL, lane, [&](int x, uint32_t e, bool valid) {
-                uint32_t c;
-                const int col = bL_entry(x, e, valid, c);
-                emit4v<C>(H, g, La[x] >> 2, x, c, col, lane);
-            });
-        } else {
-            for (int x = 0; x < nL; x++) {
-                const List bl = list_at(g, La, x, st->LL, st->LS, st->lok);
-                for (int base = 0; base < bl.len; base += 32) {
-                    const int p = base + lane;
-                    uint32_t c;
-                    const int col = bL_entry(x, p < bl.len ? bl.p[p] : 0u, p < bl.len, c);
-                    emit4<C>(H, g, La[x] >> 2, c, col, lane);
-                }
-                if (g.big) flush_hist<C>(H, g, r, a, lane);
+    if (st->lok) gather_wait();   // the L_x lists' copies (issued before the filter build)
+    // an entry e of u = L_x[q]'s list
+    auto u_entry = [&](int q, uint32_t e, bool valid, uint32_t &y) -> int {
+        y = e >> 2;
+        if (!valid || y <= r || y == x) return kNone;
+        const uint32_t eu = La[q], u = eu >> 2, w = eu & 3u;
+        const int pos = fmay(FR, y) ? find_rank(R, D, y) : -1;
+        if (pos >= 0) {   // u ~ R[j]
+            const uint32_t kj = key(pos);
+            if (pos > i) {   // part-1 event: code(R[j], u) = swap(code(u, R[j]))
+                const uint32_t mp = p1_mask(Y, kj, w);
+                const uint32_t ce = lut[mp | swap2(e & 3u) << 10], pl = lut[mp];
+                acc_add(accp(g, u, ce), 1u);
+                acc_add(accp(g, y, ce), 1u);
+                acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
+                acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                atomicAdd(H + ce, 1u);
+                atomicAdd(H + pl, 0xffffffffu);
+            } else {         // part 2: the set belongs to R[j]'s task
+                const uint32_t pl = lut[p2_mask(Y, kj, w)];
+                acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
+                acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                atomicAdd(H + pl, 0xffffffffu);
             }
+            return kNone;
         }
-        __syncwarp();
+        const uint32_t mb = Y | w << 6;
+        const int qq = fmay(FL, y) ? find_rank(La, nL, y) : -1;
+        if (qq >= 0) {
+            if (qq > q) {   // "1+2" with a u-y edge: event
+                const uint32_t mp = mb | (La[qq] & 3u) << 8;
+                const uint32_t ce = lut[mp | (e & 3u) << 10], pl = lut[mp];
+                acc_add(accp(g, u, ce), 1u);
+                acc_add(accp(g, y, ce), 1u);
+                acc_addw(accp(g, u, pl), (AccT)0 - (AccT)1);
+                acc_addw(accp(g, y, pl), (AccT)0 - (AccT)1);
+                atomicAdd(H + ce, 1u);
+                atomicAdd(H + pl, 0xffffffffu);
+            }
+            return kNone;
+        }
+        return lut[mb | (e & 3u) << 10];   // "1+1+1" {r, x, u, y}
+    };
+    if (st->lok && nL > 0) {
+        flat_walk(st->LL, st->LS, 0, nL, lane, [&](int q, uint32_t e, bool valid) {
+            uint32_t y;
+            const int col = u_entry(q, e, valid, y);
+            emit4v<C>(H, g, La[q] >> 2, q, y, col, lane);
+        });
+    } else {
+        for (int q = 0; q < nL; q++) {
+            const List ul = list_at(g, La, q, st->LL, st->LS, st->lok);
+            for (int base = 0; base < ul.len; base += 32) {
+                const int p = base + lane;
+                uint32_t y;
+                const int col = u_entry(q, p < ul.len ? ul.p[p] : 0u, p < ul.len, y);
+                emit4<C>(H, g, La[q] >> 2, y, col, lane);
+            }
+            if (g.big) flush_hist<C>(H, g, r, x, lane);
+        }
     }
-    // r and a: the plain pairs -- "3" per key pair, "2+1" with c in L_a per (key, w), "1+2" per w pair
-    for (int idx = lane; idx < 256 + 48 + 16; idx += 32) {
+    __syncwarp();
+    // r and x: the plain pairs -- "3" per key pair, "2+1" per (part, key, w), "1+2" per w pair
+    for (int idx = lane; idx < 256 + 96 + 16; idx += 32) {
         uint64_t cnt = 0;
         uint32_t mask = 0;
         if (idx < 256) {
@@ -1553,14 +1565,15 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
                 cnt = k1 < k2 ? n1 * n2 : n1 * (n1 - 1) / 2;
                 mask = star_mask(Y, k1, k2);
             }
-        } else if (idx < 256 + 48) {
-            const uint32_t k = (uint32_t)(idx - 256) / 3u, w = (uint32_t)(idx - 256) % 3u + 1u;
-            if ((P >> k) & 1u) {
-                cnt = (uint64_t)N[k] * (uint64_t)M[w];
-                mask = p1_mask(Y, k, w);
+        } else if (idx < 256 + 96) {
+            const uint32_t part = (uint32_t)(idx - 256) / 48u, rest = (uint32_t)(idx - 256) % 48u;
+            const uint32_t k = rest / 3u, w = rest % 3u + 1u;
+            if ((PP >> (16u * part + k)) & 1u) {
+                cnt = (uint64_t)N[16u * part + k] * (uint64_t)M[w];
+                mask = part == 0 ? p1_mask(Y, k, w) : p2_mask(Y, k, w);
             }
         } else {
-            const uint32_t w1 = (uint32_t)(idx - 304) >> 2, w2 = (uint32_t)(idx - 304) & 3u;
+            const uint32_t w1 = (uint32_t)(idx - 352) >> 2, w2 = (uint32_t)(idx - 352) & 3u;
             if (w1 >= 1 && w1 <= w2 && w2 <= 3) {
                 const uint64_t m1 = (uint64_t)M[w1], m2 = (uint64_t)M[w2];
                 cnt = w1 < w2 ? m1 * m2 : m1 * (m1 - (m1 > 0)) / 2;
@@ -1570,7 +1583,7 @@ __device__ __forceinline__ void light_task_closed(const Dev &g, const uint8_t *l
         if (cnt) {
             const uint32_t col = lut[mask];
             acc_addw(accp(g, r, col), (AccT)cnt);
-            acc_addw(accp(g, a, col), (AccT)cnt);
+            acc_addw(accp(g, x, col), (AccT)cnt);
         }
     }
 }
@@ -1630,7 +1643,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
         // than the idle lanes of short lists)
         const int nu = (VDMC_SKIPF(g) & 4) ? 0 : nL;
         const int nstar = rem >= 2 ? (rem + kSPW - 1) / kSPW : 0;
-        const int nj = (VDMC_SKIPF(g) & 2) || nL == 0 ? 0 : (D + kSPW - 1) / kSPW;
+        const int nj = (VDMC_SKIPF(g) & 2) || nL == 0 || g.gM ? 0 : (D + kSPW - 1) / kSPW;
         const int total = nu + nstar + nj;
         const uint32_t P = __ballot_sync(kFull, lane < 16 && sN[lane] > 0);   // keys present beyond i
         const int64_t seg = g.hbase[r];
@@ -1812,12 +1825,15 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                                   g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs, &rix);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
-            if (K == 4 && g.fold <= 0) closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_M, Hs, tid);
+            if (K == 4 && g.fold <= 0) {
+                closed_root<C>(g, lut, r, R[i] >> 2, R[i] & 3u, s_N, s_M, Hs, tid);
+                if (g.gM && tid < 4) g.gM[(g.hbase[r] + i) * 4 + tid] = (uint32_t)s_M[tid];
+            }
             for (int q = tid; q < ((D + 15) >> 4); q += kBlock) Ba[q] = 0;
             __syncthreads();
             if (tid < 32) s_N[tid] = 0;
             if (tid < 4) s_M[tid] = 0;
-        }
+                }
     }
     __syncthreads();
     for (int q = tid; q < L.total; q += kBlock) sm[q] = 0;   // light region overlays the heavy one
@@ -1856,6 +1872,41 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             const int used = st.rok ? (int)RS[D] : 0;
             uint32_t *LL = PL + used;
             st.LL = LL;
+            // k = 4 closed form: the induced edges of N+(r) among the positions beyond the item's first
+            // task, once per item (records at the top of the pool, below kPool, growing down)
+            const bool hp = K == 4 && g.fold <= 0;
+            int nrec = 0;
+            const uint32_t *recp = nullptr;
+            if (hp) {
+                const int i0 = (int)(ta - t0);
+                const int cap = min(kRecCap, kPool - used);
+                uint32_t *rtop = PL + kPool;
+                if (i0 + 1 < D) {
+                    const uint32_t x0 = R[i0] >> 2;   // positions > i0 <=> vertices > x0
+                    auto ent = [&](int q, uint32_t e, bool valid) {
+                        const uint32_t c = e >> 2;
+                        int p = -1;
+                        if (valid && c > x0 && fmay(FR, c)) p = find_rank(R, D, c);
+                        const unsigned bal = __ballot_sync(kFull, p >= 0);
+                        const int k = nrec + __popc(bal & ((1u << lane) - 1u));
+                        if (p >= 0 && k < cap) rtop[-1 - k] = (uint32_t)q | (uint32_t)p << 8 | (e & 3u) << 16;
+                        nrec += __popc(bal);
+                    };
+                    if (st.rok) flat_walk(PL, RS, i0 + 1, D, lane, ent);
+                    else
+                        for (int q = i0 + 1; q < D; q++) {
+                            const List bl = glist(g, R[q] >> 2);
+                            for (int base = 0; base < bl.len; base += 32) {
+                                const int p = base + lane;
+                                ent(q, p < bl.len ? bl.p[p] : 0u, p < bl.len);
+                            }
+                        }
+                }
+                if (nrec <= cap) recp = rtop;
+                else nrec = 0;   // did not fit: each task walks R's lists beyond its a instead
+                __syncwarp();
+            }
+            const int lcap = kPool - used - (recp ? nrec : 0);
             for (int64_t t = ta; t < tb; t++) {
                 const int i = (int)(t - t0);
                 const uint32_t a = R[i] >> 2;
@@ -1869,22 +1920,80 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 }
                 const int nL = build_a(r, al, R, D, Ba, La, lane, FR);
                 // closed form: the L_a lists' copies stay in flight through the filter build and the b
-                // walks over R; light_task_closed waits for them before the walks over L_a
+                // key counts and the R side; light_task_hp waits for them before the walks over L_a
                 const bool closed = K == 4 && g.fold <= 0;
-                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, kPool - used, lane, !closed);
+                st.lok = K == 4 && La == Las && gather_lists(g, La, nL, LS, LO, kSmax, LL, lcap, lane, !closed);
                 FL[lane] = 0;
                 __syncwarp();
                 for (int q = lane; q < nL; q += 32) fadd(FL, La[q] >> 2);
                 __syncwarp();
-                if (K == 4 && g.fold <= 0)
-                    light_task_closed<C>(g, lut, r, i, R, D, Ba, La, nL, H, reinterpret_cast<int *>(Bb),
-                                         reinterpret_cast<int *>(FL + kFW), &st, lane);
+                if (hp)   // N: RO's words are free once R's lists are staged
+                    light_task_hp<C>(g, lut, r, i, R, D, Ba, La, nL, H, reinterpret_cast<int *>(RO),
+                                     reinterpret_cast<int *>(FL + kFW), &st, recp, nrec, lane);
                 else
                     task_loops<K, C, 1>(g, lut, r, i, R, D, Ba, La, nL, Bb, Bl, H, nullptr, nullptr, nullptr, nullptr,
                                         &st, 0, lane);
                 flush_hist<C>(H, g, r, a, lane);
                 clear_words(Ba, 0, (D + 15) >> 4, lane);
                 __syncwarp();
+            }
+        }
+    }
+}
+
+// "2+1", the R[j] side at heavy roots, once per root instead of once per task: R[j] lies in M_i[w]
+// plain sets {r, x_i, R[j], c} of class cls(Y_i, x_j, w) for every task i != j of the slice (the
+// part-1 and part-2 masks of a plain set are the same digraph, so the LUT gives one column), i.e.
+// in T[Y][w] = sum over the slice's tasks with code(r, x_i) = Y of M_i[w], less its own task's
+// M_j; an induced neighbour x_i of R[j] (k_nr's lists) puts those M_i[w] sets in the class with the
+// x_i-R[j] edge instead (exact part-1 / part-2 mask, as cross_j_closed).  M_i: written by k_enum.
+template <int C>
+__global__ void __launch_bounds__(256) k_rside(Dev g, const int32_t *__restrict__ hroots, int64_t nh, int64_t lo,
+                                               int64_t hi, const uint8_t *__restrict__ lut_g) {
+    __shared__ uint8_t lut[4096];
+    __shared__ unsigned long long T[16];   // T[Y * 4 + w]
+    for (int q = threadIdx.x; q < 4096; q += blockDim.x) lut[q] = lut_g[q];
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const uint32_t r = (uint32_t)hroots[h];
+        const int64_t rs = g.split[r], t0 = g.tfirst[r];
+        const int D = (int)(g.off[r + 1] - rs);
+        const int i0 = (int)max(lo - t0, (int64_t)0), i1 = (int)min(hi - t0, (int64_t)D);
+        if (i0 >= i1) continue;   // uniform over the CTA
+        const int64_t seg = g.hbase[r];
+        __syncthreads();
+        if (threadIdx.x < 16) T[threadIdx.x] = 0;
+        __syncthreads();
+        for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+            const uint32_t Y = g.adj[rs + i] & 3u;
+#pragma unroll
+            for (int w = 1; w <= 3; w++) {
+                const uint32_t m = g.gM[(seg + i) * 4 + w];
+                if (m) atomicAdd(T + Y * 4 + w, (unsigned long long)m);
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < D; j += blockDim.x) {
+            const uint32_t ej = g.adj[rs + j], y = ej >> 2, xj = ej & 3u;
+            const bool own = j >= i0 && j < i1;
+#pragma unroll
+            for (uint32_t Y = 1; Y <= 3; Y++)
+#pragma unroll
+                for (uint32_t w = 1; w <= 3; w++) {
+                    const unsigned long long cnt = T[Y * 4 + w] - (own && Y == xj ? g.gM[(seg + j) * 4 + w] : 0u);
+                    if (cnt) acc_addw(accp(g, y, lut[p1_mask(Y, xj, w)]), (AccT)cnt);
+                }
+            for (int64_t e = g.nr_off[seg + j], e1 = g.nr_off[seg + j + 1]; e < e1; e++) {
+                const uint32_t en = g.nr_adj[e];
+                const int i = (int)(en >> 2);
+                if (i < i0 || i >= i1) continue;
+                const uint32_t Yi = g.adj[rs + i] & 3u, kj = xj | swap2(en & 3u) << 2;
+#pragma unroll
+                for (uint32_t w = 1; w <= 3; w++) {
+                    const uint32_t m = g.gM[(seg + i) * 4 + w];
+                    if (!m) continue;
+                    acc_addw(accp(g, y, lut[p1_mask(Yi, xj, w)]), (AccT)0 - (AccT)m);
+                    acc_addw(accp(g, y, lut[j > i ? p1_mask(Yi, kj, w) : p2_mask(Yi, kj, w)]), (AccT)m);
+                }
             }
         }
     }
@@ -2362,10 +2471,21 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     d.hbase = g->hbase;
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
+    // k = 4 closed form at heavy roots: the "2+1" R[j] side per root (k_rside) from the tasks' M
+    const bool rside = K == 4 && o.star_block <= 0 && g->nheavy > 0 && g->nhroots > 0;
+    uint32_t *gM = nullptr;
+    if (rside) VDMC_CUDA(dalloc((void **)&gM, (size_t)g->nheavy * 4 * sizeof(uint32_t), s));
+    d.gM = gM;
     if (hi > lo) {
         kern<<<grid, kBlock, smem, s>>>(d, L, lo, hi, ctr, lut);
         VDMC_LAUNCH();
+        if (rside) {
+            const int rg = (int)std::min<int64_t>(g->nhroots, (int64_t)nsm * 8);
+            k_rside<C><<<rg, 256, 0, s>>>(d, g->hroots, g->nhroots, lo, hi, lut);
+            VDMC_LAUNCH();
+        }
     }
+    if (gM) dfree(gM, s);
     if (ms3) VDMC_CUDA(cudaEventRecord(ev.e[2], s));
     dfree(scratch, s);
     dfree(ctr, s);
