@@ -468,7 +468,7 @@ def roofline(args, k, motifs, enum_ms, peak, peak_src, sm_mhz):
     roof = {"bound": "alu", "kernel": f"k_enum<{k}>", "unit": "Gwarp-inst/s", "peak": peak_issue,
             "peak_source": f"148 SMs x 4 schedulers x 1 warp-instruction/clock x {sm_mhz:.0f} MHz (measured SM clock)",
             "motifs_per_launch": motifs}
-    stale = bool(c) and abs(c.get("duration_ms", 0.0) - enum_ms) > 0.15 * enum_ms
+    stale = bool(c) and abs(c.get("duration_ms", 0.0) - enum_ms) > 0.08 * enum_ms
     if c and "warp_insts" in c and not stale:
         achieved = c["warp_insts"] / t / 1e9
         atoms = c["l2_red_requests"] + c.get("l2_atom_requests", 0)

@@ -62,7 +62,9 @@ constexpr int kLightDeg = 128;        // light root: G_U degree <= this (measure
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
-constexpr int kHChunk = 8;            // heavy tasks fetched per CTA request
+constexpr int kHChunk = 32;           // heavy tasks fetched per CTA request (<= 32: one warp classifies them)
+constexpr int kWL = 256;              // heavy warp-mode task: a's list length at most this (its L_a slot)
+constexpr int kWRem = 1024;           // heavy warp-mode task: at most this many positions beyond a
 constexpr int kLightChunk = 8;        // light items: at most this many tasks of one root (a root of ~100
                                       // tasks is ~15 ms of one warp: cut, it no longer bounds a slice)
 
@@ -119,6 +121,8 @@ struct Layout {
     int light;                    // light region: per warp kLightWords
     int total;                    // words
     int T;                        // heavy: bucket index of R (u16 positions, kBuckets + 1 of them), or -1
+    int NB;                       // heavy: bit q = position q of R has an induced neighbour (k_nr lists)
+    int W, ws, wm;                // heavy: per-warp slots of the warp-mode tasks (overlay La..Bl), stride, enabled
 };
 constexpr int kLW = kLightDeg;               // light list capacity
 constexpr int kLB = (kLightDeg + 15) / 16;   // light bitmap words
@@ -376,7 +380,7 @@ __device__ __forceinline__ List list_at(const Dev &g, const uint32_t *V, int q, 
 // Phase A of a task: scatter code(a, x) for x in R into Ba; collect L_a (sorted) into La.
 // al = a's list.  Run by one warp.  Returns |L_a|.
 __device__ int build_a(uint32_t r, List al, const uint32_t *R, int D, uint32_t *Ba, uint32_t *La, int lane,
-                       const uint32_t *FR) {
+                       const uint32_t *FR, const RIndex *ix = nullptr) {
     int nL = 0;
     for (int base = 0; base < al.len; base += 32) {
         const int p = base + lane;
@@ -386,7 +390,7 @@ __device__ int build_a(uint32_t r, List al, const uint32_t *R, int D, uint32_t *
             e = al.p[p];
             const uint32_t x = e >> 2;
             if (x > r) {
-                const int pos = fmay(FR, x) ? find_rank(R, D, x) : -1;
+                const int pos = ix ? find_pos(R, D, x, *ix) : (fmay(FR, x) ? find_rank(R, D, x) : -1);
                 if (pos >= 0) set2(Ba, pos, e & 3u);
                 else keep = true;
             }
@@ -708,15 +712,16 @@ template <int C>
 __device__ __forceinline__ void star_closed_item(const Dev &g, const uint8_t *lut, unsigned long long *Hs,
                                                  uint32_t cra, int i, const uint32_t *R, int D,
                                                  const uint8_t *codes, const int *sN, uint32_t P, int64_t seg,
-                                                 int q0, int lane) {
+                                                 int q0, int lane, const uint32_t *NB) {
 #pragma unroll 1
     for (int t = 0; t < kSPM; t++) {
         const int q = q0 + 32 * t + lane;
         if (q >= D) break;   // no warp-collective operations below
         const uint32_t v = R[q] >> 2, kq = codes[q];
         uint64_t corr = 0;   // induced neighbours beyond i with keys 1..3 (al = 0), 21-bit fields
-        int64_t e = g.nr_off[seg + q];
-        const int64_t e1 = g.nr_off[seg + q + 1];
+        const bool has = (NB[q >> 5] >> (q & 31)) & 1u;   // most positions have none: no list bounds read
+        int64_t e = has ? g.nr_off[seg + q] : 0;
+        const int64_t e1 = has ? g.nr_off[seg + q + 1] : 0;
         if (e1 - e > 16) {   // first entry with position > i (the list ascends in position)
             int64_t lo = e, hi = e1;
             while (lo < hi) {
@@ -1403,14 +1408,22 @@ __device__ __forceinline__ bool ca_build(const Dev &g, uint32_t r, int i, const 
 // R[j] side of "3" (j > i) and "2+1" (all j != i); the c side of "2+1" / "1+2" for c in L_x; one
 // walk per u in L_x (part-1 events and part-2 removals for u ~ R[j], "1+2" events, "1+1+1"
 // sets); the plain pairs of r and x.  N: 32 ints, M: 4 ints of the warp's scratch.
-template <int C>
+// HV: a small task of a heavy root run by one warp (R is the CTA's staged N+(r)): positions by the
+// bucket index ix, the "3" induced edges from k_nr's lists (NB: positions that have any), and the
+// "2+1" R[j] side left to k_rside (this task's M goes to gMt[0..3]).
+template <int C, bool HV = false>
 __device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, uint32_t r, int i,
                                               const uint32_t *R, int D, const uint32_t *Ba, const uint32_t *La,
                                               int nL, uint32_t *H, int *N, int *M, const Staged *st,
-                                              const uint32_t *rec, int nrec, int lane) {
+                                              const uint32_t *rec, int nrec, int lane, const RIndex *ix = nullptr,
+                                              int64_t seg = 0, const uint32_t *NB = nullptr, uint32_t *gMt = nullptr) {
     const uint32_t Y = R[i] & 3u, x = R[i] >> 2;
     const uint32_t *FR = st->FR, *FL = st->FL;
     auto key = [&](int q) -> uint32_t { return (R[q] & 3u) | get2(Ba, q) << 2; };
+    auto rpos = [&](uint32_t y) -> int {   // position of vertex y in R, or -1
+        if constexpr (HV) return find_pos(R, D, y, *ix);
+        else return fmay(FR, y) ? find_rank(R, D, y) : -1;
+    };
     N[lane] = 0;
     if (lane < 4) M[lane] = 0;
     __syncwarp();
@@ -1429,6 +1442,7 @@ __device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, 
     __syncwarp();
     const uint32_t PP = __ballot_sync(kFull, N[lane] > 0);   // slots present (beyond | before << 16)
     const uint32_t P = PP & 0xffffu;
+    if (HV && lane < 4) gMt[lane] = (uint32_t)M[lane];
     // "3": an induced edge R[q] - R[p] (q, p > i) is not a plain partner of R[q]; q < p: the event
     // {r, x, R[q], R[p]}, classified by its full mask
     auto rec_act = [&](int q, int p, uint32_t z) {
@@ -1443,7 +1457,16 @@ __device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, 
             atomicAdd(H + pl, 0xffffffffu);
         }
     };
-    if (rec) {
+    if constexpr (HV) {
+        for (int q = i + 1 + lane; q < D; q += 32) {   // no warp-collective operations inside
+            if (!((NB[q >> 5] >> (q & 31)) & 1u)) continue;
+            for (int64_t e = g.nr_off[seg + q], e1 = g.nr_off[seg + q + 1]; e < e1; e++) {
+                const uint32_t en = g.nr_adj[e];
+                const int p = (int)(en >> 2);
+                if (p > i) rec_act(q, p, en & 3u);
+            }
+        }
+    } else if (rec) {
         for (int t = lane; t < nrec; t += 32) {
             const uint32_t v = rec[-1 - t];
             const int q = (int)(v & 0xffu), p = (int)((v >> 8) & 0xffu);
@@ -1475,9 +1498,10 @@ __device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, 
                 const uint32_t cnt = (uint32_t)N[k] - (k == kb ? 1u : 0u);
                 if (cnt) acc_add(accp(g, b, lut[star_mask(Y, kb, k)]), cnt);
             }
+        if (!HV)   // (heavy roots: k_rside)
 #pragma unroll
-        for (uint32_t w = 1; w <= 3; w++)
-            if (M[w]) acc_add(accp(g, b, lut[j > i ? p1_mask(Y, kb, w) : p2_mask(Y, kb, w)]), (uint32_t)M[w]);
+            for (uint32_t w = 1; w <= 3; w++)
+                if (M[w]) acc_add(accp(g, b, lut[j > i ? p1_mask(Y, kb, w) : p2_mask(Y, kb, w)]), (uint32_t)M[w]);
     }
     // c in L_x (lanes): plain "2+1" sets per (part, key), plain "1+2" sets per partner code
     for (int q = lane; q < nL; q += 32) {
@@ -1498,7 +1522,7 @@ __device__ __forceinline__ void light_task_hp(const Dev &g, const uint8_t *lut, 
         y = e >> 2;
         if (!valid || y <= r || y == x) return kNone;
         const uint32_t eu = La[q], u = eu >> 2, w = eu & 3u;
-        const int pos = fmay(FR, y) ? find_rank(R, D, y) : -1;
+        const int pos = rpos(y);
         if (pos >= 0) {   // u ~ R[j]
             const uint32_t kj = key(pos);
             if (pos > i) {   // part-1 event: code(R[j], u) = swap(code(u, R[j]))
@@ -1598,7 +1622,7 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                                            uint32_t *Bl, uint32_t *H, const uint8_t *codes, int *wctr, uint32_t *ca,
                                            int *s_ca, const Staged *st, int w, int lane, const int *sN = nullptr,
                                            const int *sM = nullptr, unsigned long long *Hs = nullptr,
-                                           const RIndex *ix = nullptr) {
+                                           const RIndex *ix = nullptr, const uint32_t *NB = nullptr) {
     const uint32_t ea = R[i], a = ea >> 2, cra = ea & 3u;
     if constexpr (K == 3) {
         // "2": b in R after a.   mask (r,a) | (r,b) << 2 | (a,b) << 4
@@ -1657,7 +1681,8 @@ __device__ __forceinline__ void task_loops(const Dev &g, const uint8_t *lut, uin
                 if (g.big) flush_hist<C>(H, g, r, a, lane);
             } else if (it < nu + nstar) {
                 if (!(VDMC_SKIPF(g) & 1))
-                    star_closed_item<C>(g, lut, Hs, cra, i, R, D, codes, sN, P, seg, i + 1 + (it - nu) * kSPW, lane);
+                    star_closed_item<C>(g, lut, Hs, cra, i, R, D, codes, sN, P, seg, i + 1 + (it - nu) * kSPW, lane,
+                                        NB);
             } else {
                 cross_j_closed<C>(g, lut, cra, i, R, D, codes, sM, (it - nu - nstar) * kSPW, lane);
             }
@@ -1719,6 +1744,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     __shared__ uint8_t lut[NM];
     __shared__ int64_t s_item, s_sub[4];   // s_sub: the slice's heavy_task [h0, h1) and light_root [l0, l1)
     __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
+    __shared__ unsigned s_wm;               // heavy: warp-mode tasks of the fetched chunk (bit per task)
+    __shared__ int32_t s_wr[kHChunk];       // heavy: their roots
     __shared__ int s_N[32], s_M[4];         // closed forms: key counts beyond / before i, |L_x| per code(x, c)
     __shared__ unsigned long long Hs[C];    // closed forms: r / x side of events and take-backs (modular)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1761,6 +1788,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         __syncthreads();
         int64_t staged = -1;
         RIndex rix{0u, 0u, 0, nullptr};
+        const bool wmode = HSMEM && K == 4 && L.wm && g.fold <= 0 && g.gM != nullptr;
         int64_t h = 0, hend = 0;
         for (;;) {   // bounds re-read from shared memory (keeps them out of the loop's registers)
             if (h >= hend) {   // kHChunk consecutive tasks per fetch: one R staging for a small root's
@@ -1769,9 +1797,79 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
                 h = s_item;
                 hend = h + kHChunk;
+                if (wmode && wid == 0) {   // warp-mode tasks: a's list fits the warp's slot, few positions beyond a
+                    const int64_t x = h + lane;
+                    bool wm = false;
+                    int32_t rr = -1;
+                    if (lane < kHChunk && x < s_sub[1]) {
+                        const int64_t t = g.heavy_task[x];
+                        rr = g.task_root[t];
+                        const int64_t rs = g.split[rr];
+                        const int i = (int)(t - g.tfirst[rr]), D = (int)(g.off[rr + 1] - rs);
+                        const uint32_t a = g.adj[rs + i] >> 2;
+                        wm = D - i - 1 <= kWRem && g.off[a + 1] - g.off[a] <= kWL;
+                    }
+                    const unsigned m = __ballot_sync(kFull, wm);
+                    if (lane < kHChunk) s_wr[lane] = rr;
+                    if (lane == 0) s_wm = m;
+                }
                 __syncthreads();
             }
             if (h >= s_sub[1]) break;
+            // stage N+(r) (once per root): R, NB (positions with an induced neighbour), the bucket index
+            auto stage = [&](uint32_t r) {
+                const int64_t rs = g.split[r];
+                const int D = (int)(g.off[r + 1] - rs);
+                for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
+                if (K == 4 && g.fold <= 0) {
+                    const int64_t seg = g.hbase[r];
+                    for (int base = wid * 32; base < D; base += kBlock) {
+                        const int q = base + lane;
+                        const unsigned m = __ballot_sync(kFull, q < D && g.nr_off[seg + q + 1] > g.nr_off[seg + q]);
+                        if (lane == 0) hb[L.NB + (base >> 5)] = m;
+                    }
+                }
+                staged = r;
+                __syncthreads();
+                rix = build_rindex(R, D, L.T >= 0 && g.fold <= 0 ? reinterpret_cast<uint16_t *>(hb + L.T) : nullptr,
+                                   tid, kBlock);
+                __syncthreads();
+            };
+            if (wmode && ((s_wm >> (int)(h - s_item)) & 1u)) {
+                // a run of warp-mode tasks of one root: one warp per task (light_task_hp<HV>), in snake order
+                // over the warps (the run's tasks shrink along it)
+                const uint32_t r = (uint32_t)s_wr[h - s_item];
+                int64_t h2 = h + 1;
+                while (h2 < hend && h2 < s_sub[1] && ((s_wm >> (int)(h2 - s_item)) & 1u) &&
+                       (uint32_t)s_wr[h2 - s_item] == r)
+                    h2++;
+                if (staged != r) stage(r);
+                const int64_t rs = g.split[r], seg = g.hbase[r], tf = g.tfirst[r];
+                const int D = (int)(g.off[r + 1] - rs), n = (int)(h2 - h);
+                uint32_t *ws = hb + L.W + wid * L.ws;
+                uint32_t *wBa = ws, *wLa = ws + L.bw, *wN = wLa + kWL, *wM = wN + 32, *wFL = wM + 4;
+                for (int k = 0; k * kWarps < n; k++) {
+                    const int idx = (k & 1) ? (k + 1) * kWarps - 1 - wid : k * kWarps + wid;
+                    if (idx >= n) continue;
+                    const int i = (int)(g.heavy_task[h + idx] - tf);
+                    clear_words(wBa, 0, (D + 15) >> 4, lane);
+                    __syncwarp();
+                    const List al = glist(g, R[i] >> 2);
+                    const int nL = build_a(r, al, R, D, wBa, wLa, lane, nullptr, &rix);
+                    wFL[lane] = 0;
+                    __syncwarp();
+                    for (int q = lane; q < nL; q += 32) fadd(wFL, wLa[q] >> 2);
+                    __syncwarp();
+                    const Staged st{nullptr, nullptr, nullptr, nullptr, false, false, nullptr, wFL};
+                    light_task_hp<C, true>(g, lut, r, i, R, D, wBa, wLa, nL, H, reinterpret_cast<int *>(wN),
+                                           reinterpret_cast<int *>(wM), &st, nullptr, 0, lane, &rix, seg, hb + L.NB,
+                                           g.gM + (seg + i) * 4);
+                    flush_hist<C>(H, g, r, R[i] >> 2, lane);
+                }
+                __syncthreads();
+                h = h2;
+                continue;
+            }
             const int64_t t = g.heavy_task[h++];
             const uint32_t r = (uint32_t)g.task_root[t];
             const int64_t rs = g.split[r];
@@ -1780,14 +1878,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
 #ifdef VDMC_PROFILING
             if (g.minrem > 0 ? D - i - 1 < g.minrem : (g.minrem < 0 && D - i - 1 >= -g.minrem)) continue;   // VDMC_MINREM
 #endif
-            if (staged != r) {
-                for (int q = tid; q < D; q += kBlock) R[q] = g.adj[rs + q];
-                staged = r;
-                __syncthreads();
-                rix = build_rindex(R, D, L.T >= 0 && g.fold <= 0 ? reinterpret_cast<uint16_t *>(hb + L.T) : nullptr,
-                                   tid, kBlock);
-                __syncthreads();
-            }
+            if (staged != r) stage(r);
             const List al = glist(g, R[i] >> 2);
             build_a_cta<kWarps>(r, al, R, D, Ba, La, hb + L.Bl, &s_nL, wid, lane, rix);
             const int nL = s_nL;
@@ -1822,7 +1913,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
             }
             __syncthreads();
             task_loops<K, C, kWarps>(g, lut, r, i, R, D, Ba, La, nL, nullptr, Bl, H, codes, &s_work,
-                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs, &rix);
+                                  g.gca + (int64_t)blockIdx.x * g.gca_per_cta, s_ca, nullptr, wid, lane, s_N, s_M, Hs, &rix,
+                                  hb + L.NB);
             flush_hist<C>(H, g, r, R[i] >> 2, lane);
             __syncthreads();
             if (K == 4 && g.fold <= 0) {
@@ -2200,21 +2292,29 @@ Layout make_layout(int maxdeg, int C, bool &heavy_in_smem, int64_t &per_cta_word
     L.lw = (md + 15) / 16;
     // heavy buffers (offsets relative to the heavy base)
     L.R = 0;
-    L.La = L.R + md;
-    L.Ba = L.La + md;
-    L.Bb = L.Ba + L.bw;                  // heavy: the per-task code bytes (md bytes)
+    L.T = L.R + md;                      // bucket index of R: (kBuckets + 1) u16
+    L.NB = L.T + (kBuckets + 2) / 2;
+    L.Ba = L.NB + (md + 31) / 32;
+    L.La = L.Ba + L.bw;
+    L.Bb = L.La + md;                    // heavy: the per-task code bytes (md bytes)
     L.Bl = L.Bb + (md + 3) / 4;
-    L.T = L.Bl + kWarps * L.lw;          // bucket index of R: (kBuckets + 1) u16
-    const int heavy_words = L.T + (kBuckets + 2) / 2;
+    const int cta_words = L.Bl + kWarps * L.lw;
+    // warp-mode slots (per warp: Ba[bw] | La[kWL] | N[32] | M[4] | FL[kFW]) overlay La .. Bl
+    L.W = L.La;
+    L.ws = L.bw + kWL + 32 + 4 + kFW;
+    const int warp_words = L.W + kWarps * L.ws;
     const int light_words = kWarps * kLightWords;
     const int hist_words = kWarps * C;
     const int budget_words = (104 * 1024) / 4 - hist_words;   // keep 2 CTAs per SM
-    heavy_in_smem = heavy_words <= budget_words && !force_global;
-    const int region = std::max(light_words, heavy_in_smem ? heavy_words : 0);
+    const int heavy_words = std::max(cta_words, warp_words);
+    L.wm = heavy_words <= budget_words && !force_global;   // warp mode only with the heavy buffers in smem
+    const int hw = L.wm ? heavy_words : cta_words;
+    heavy_in_smem = hw <= budget_words && !force_global;
+    const int region = std::max(light_words, heavy_in_smem ? hw : 0);
     L.light = 0;
     L.hist = region;
     L.total = region + hist_words;
-    per_cta_words = heavy_in_smem ? 0 : heavy_words;
+    per_cta_words = heavy_in_smem ? 0 : hw;
     return L;
 }
 
