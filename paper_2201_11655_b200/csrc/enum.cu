@@ -63,8 +63,8 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
 constexpr int kHChunk = 32;           // heavy tasks fetched per CTA request (<= 32: one warp classifies them)
-constexpr int kWL = 256;              // heavy warp-mode task: a's list length at most this (its L_a slot)
-constexpr int kWRem = 1024;           // heavy warp-mode task: at most this many positions beyond a
+constexpr int kWL = 256;              // heavy warp-mode task: a's list length at most this (its L_a slot;
+                                      // measured 64 / 128 / 256 / 512: 256 best)
 constexpr int kLightChunk = 8;        // light items: at most this many tasks of one root (a root of ~100
                                       // tasks is ~15 ms of one warp: cut, it no longer bounds a slice)
 
@@ -1797,7 +1797,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                 __syncthreads();
                 h = s_item;
                 hend = h + kHChunk;
-                if (wmode && wid == 0) {   // warp-mode tasks: a's list fits the warp's slot, few positions beyond a
+                if (wmode && wid == 0) {   // warp-mode tasks: a's list fits the warp's slot
                     const int64_t x = h + lane;
                     bool wm = false;
                     int32_t rr = -1;
@@ -1805,9 +1805,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
                         const int64_t t = g.heavy_task[x];
                         rr = g.task_root[t];
                         const int64_t rs = g.split[rr];
-                        const int i = (int)(t - g.tfirst[rr]), D = (int)(g.off[rr + 1] - rs);
-                        const uint32_t a = g.adj[rs + i] >> 2;
-                        wm = D - i - 1 <= kWRem && g.off[a + 1] - g.off[a] <= kWL;
+                        const uint32_t a = g.adj[rs + (t - g.tfirst[rr])] >> 2;
+                        wm = g.off[a + 1] - g.off[a] <= kWL;   // (a positions limit measured slower)
                     }
                     const unsigned m = __ballot_sync(kFull, wm);
                     if (lane < kHChunk) s_wr[lane] = rr;
@@ -2173,12 +2172,11 @@ __global__ void k_cost(int64_t ntasks, int k, const int64_t *__restrict__ off, c
         if (k == 3) {
             const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
             c = heavy ? 92290 + 50 * (rem + da) : 1454 + 10 * (rem + nla) + suf + s2[a] / 8;
-        } else if (heavy) {   // k = 4 closed-form heavy task (units of 1e-9 ms; tools/fit_plan.py, profiles/r02_planner_fit.txt):
-                              // per-task overhead (barriers, phase A), O(D) items, walks of L_a
-            c = 21090 + D * 2452 / 100 + nla * 871;
-        } else {              // light task: b-in-R walks (suffix of forward degrees), L_a walks, per-root staging
-            const int64_t suf = fsum[tfirst[r + 1] - 1] - fsum[t];
-            c = suf * 3614 / 100 + nla * 104 + (ia == rs ? 3898 : 0);
+        } else if (heavy) {   // k = 4 heavy task (units of 1e-12 ms; tools/fit_plan.py, profiles/r02n_planner_fit.txt)
+            c = da <= kWL ? 14954100 + 34100 * D   // one warp (light closed form over the staged R)
+                          : 760 * D * da;          // one CTA (phase A over a's list, O(D) items, walks of L_a)
+        } else {              // light task: O(D) key counts and R side, L_a walks, per-item staging of R's lists
+            c = 146800 * D + 127200 * nla + ((ia - rs) % kLightChunk == 0 ? 2340700 : 0);
         }
         cost[t] = c;
     }

@@ -14,8 +14,8 @@ from scipy.optimize import nnls
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import graphgen as G  # noqa: E402
 
-NAMES = ["h_cnt", "h_D", "h_nla", "h_s2a", "h_rem", "h_root",
-         "l_cnt", "l_suf", "l_s2a", "l_nla", "l_rem", "l_root", "l_rootsuf", "l_suf_unstaged"]
+NAMES = ["h_cnt", "h_D", "h_nla", "h_s2a", "h_rem", "h_Dda", "w_cnt", "w_D", "w_rem", "w_s2a",
+         "l_cnt", "l_D", "l_nla", "l_s2a", "l_item", "l_itemsuf"]
 
 
 def task_features(name):
@@ -54,13 +54,18 @@ def task_features(name):
     nla = (off[ta + 1] - pos).astype(np.float64)         # a's neighbours with rank > r
     heavy = degr[tr] > 128
     Dd = D[tr].astype(np.float64)
-    first = (i == 0) * 1.0
-    h, l = heavy * 1.0, (~heavy) * 1.0
-    staged = (Dd <= 64) & (rootsum <= 896)          # the light warp stages R's lists (kSmax, kPool)
-    F = np.stack([h, h * Dd, h * nla, h * S2[ta], h * rem, h * first * Dd,
-                  l, l * suf, l * S2[ta], l * nla, l * rem, l * first, l * first * rootsum,
-                  l * suf * (~staged)], axis=1)
+    warp = heavy & (da <= 256)                     # heavy tasks run one per warp (enum.cu kWL)
+    cta = heavy & ~warp
+    h, w, l = cta * 1.0, warp * 1.0, (~heavy) * 1.0
+    item = (i % 8 == 0) * 1.0                      # light items: <= 8 tasks (kLightChunk)
+    F = np.stack([h, h * Dd, h * nla, h * S2[ta], h * rem, h * Dd * da / 1e3, w, w * Dd, w * rem, w * S2[ta],
+                  l, l * Dd, l * nla, l * S2[ta], l * item, l * item * (suf + da)], axis=1)
     return F, heavy
+
+
+def cxx(coef):
+    """k_cost constants: ms per unit -> integer units of 1e-12 ms"""
+    return {nm: int(round(c * 1e12)) for nm, c in zip(NAMES, coef)}
 
 
 def main():
@@ -92,7 +97,8 @@ def main():
     for nm, c in zip(NAMES + ["intercept"], coef):
         print(f"{nm:10s} {c:.4g}")
     print("rel err per row:", np.round((pred - y) / y, 3))
-    print("ns per unit (k_cost integer weights, x1e6 ms -> ns):", {nm: round(c * 1e6, 3) for nm, c in zip(NAMES, coef)})
+    print("ns per unit:", {nm: round(c * 1e6, 4) for nm, c in zip(NAMES, coef)})
+    print("k_cost integer weights (1e-12 ms):", cxx(coef))
 
 
 if __name__ == "__main__":

@@ -8,3 +8,4 @@ for c in cfg4 cfg5; do
     timeout 900 python bench.py --config $c --virtual-parts $G --steps 2 > $O/vparts_${c}_$G.json 2> $O/vparts_${c}_$G.err
   done
 done
+timeout 1500 python -m pytest tests -m gpu -x -q -rf > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
