@@ -15,12 +15,16 @@
 // Every connected set with minimum r falls in exactly one case, once.
 //
 // Work unit ("each pair of a vertex and one of its neighbors"): the task (r, a).
-//   * heavy roots (deg(r) > kLightDeg): one CTA per task; the 16 warps split the loops over
-//     b.  R and L_a live in shared memory (global scratch if the graph's degree is too big).
-//   * light roots: one warp per root, its tasks in sequence; R and L_a in the warp's smem.
+//   * heavy roots (deg(r) > kLightDeg): the CTA stages R = N+(r) once per root; a task whose a
+//     has a short list (<= kWL) runs on one warp (light_task_hp<HV>, 16 tasks in flight per
+//     CTA), the others on the whole CTA (the 16 warps split its items).  R and L_a live in
+//     shared memory (global scratch if the graph's degree is too big).
+//   * light roots: one warp per item (<= kLightChunk tasks of one root), its tasks in sequence;
+//     R, L_a and their staged lists in the warp's smem.
 //   One persistent kernel: CTAs drain the heavy task list (ordered by rank = degree
 //   descending, then by a's position: longest first), then their warps drain the light
-//   roots.  Both lists come from a global atomic counter.
+//   items.  Both lists come from a global atomic counter.  k = 4 default: closed forms
+//   (DESIGN §3b), the "2+1" R[j] side of heavy roots summed per root by k_rside.
 // Membership tests are binary searches in the staged sorted lists (shared memory).  The
 // codes (a, x) and (b, x) for x in R or L_a are scattered once into 2-bit-per-position
 // bitmaps, so the innermost loops (one set per lane) read only shared memory.
