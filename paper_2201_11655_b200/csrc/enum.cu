@@ -67,6 +67,8 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNone = 255;
 constexpr int kPF = 2;                // light walks: list entries per lane loaded ahead
 constexpr int kHChunk = 32;           // heavy tasks fetched per CTA request (<= 32: one warp classifies them)
+constexpr int kHubDeg = 1024;         // heavy tasks of the leading roots above this degree (a prefix of the heavy
+constexpr int kHubChunk = 16;         // list under the degree order) are fetched kHubChunk per request
 constexpr int kWL = 256;              // heavy warp-mode task: a's list length at most this (its L_a slot;
                                       // measured 64 / 128 / 256 / 512: 256 best)
 constexpr int kLightChunk = 8;        // light items: at most this many tasks of one root (a root of ~100
@@ -113,6 +115,7 @@ struct Dev {
     const int64_t *__restrict__ hbase;        // heavy root -> segment of nr_off
     const int64_t *__restrict__ nr_off;       // induced adjacency of N+(r), position space
     const uint32_t *__restrict__ nr_adj;
+    int64_t hub_tasks;                        // heavy tasks of the leading roots of degree > kHubDeg
     uint32_t *__restrict__ gM;                // closed forms, heavy tasks: M[w] per task at (hbase[r] + i) * 4 + w;
                                               // the "2+1" R[j] side is then added per root by k_rside
 };
@@ -1749,6 +1752,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
     __shared__ int64_t s_item, s_sub[4];   // s_sub: the slice's heavy_task [h0, h1) and light_root [l0, l1)
     __shared__ int s_nL, s_work, s_ca[2];   // s_ca: CA space used, next c of ca_build
     __shared__ unsigned s_wm;               // heavy: warp-mode tasks of the fetched chunk (bit per task)
+    __shared__ int s_cnt;                   // heavy: tasks in the fetched chunk
     __shared__ int32_t s_wr[kHChunk];       // heavy: their roots
     __shared__ int s_N[32], s_M[4];         // closed forms: key counts beyond / before i, |L_x| per code(x, c)
     __shared__ unsigned long long Hs[C];    // closed forms: r / x side of events and take-backs (modular)
@@ -1797,15 +1801,20 @@ __global__ void __launch_bounds__(kBlock, 2) k_enum(Dev g, Layout L, int64_t lo,
         for (;;) {   // bounds re-read from shared memory (keeps them out of the loop's registers)
             if (h >= hend) {   // kHChunk consecutive tasks per fetch: one R staging for a small root's
                                // tasks, and two barriers per chunk instead of per task
-                if (tid == 0) s_item = s_sub[0] + (int64_t)atomicAdd(ctr, (unsigned long long)kHChunk);
+                if (tid == 0) {   // chunk k: kHubChunk tasks over the hub prefix of the slice, then kHChunk
+                    const int64_t k = (int64_t)atomicAdd(ctr, 1ull);
+                    const int64_t K1 = (g.hub_tasks + kHubChunk - 1) / kHubChunk;
+                    s_item = s_sub[0] + (k < K1 ? k * kHubChunk : K1 * kHubChunk + (k - K1) * kHChunk);
+                    s_cnt = k < K1 ? kHubChunk : kHChunk;
+                }
                 __syncthreads();
                 h = s_item;
-                hend = h + kHChunk;
+                hend = h + s_cnt;
                 if (wmode && wid == 0) {   // warp-mode tasks: a's list fits the warp's slot
                     const int64_t x = h + lane;
                     bool wm = false;
                     int32_t rr = -1;
-                    if (lane < kHChunk && x < s_sub[1]) {
+                    if (x < hend && x < s_sub[1]) {
                         const int64_t t = g.heavy_task[x];
                         rr = g.task_root[t];
                         const int64_t rs = g.split[rr];
@@ -2275,6 +2284,13 @@ __global__ void k_heavy_d(int64_t nh, const int32_t *__restrict__ hroots, const 
     }
 }
 
+__global__ void k_hub_prefix(int64_t nh, const int32_t *__restrict__ hroots, const int64_t *__restrict__ off,
+                             unsigned long long *__restrict__ firstq) {   // first heavy root of degree <= kHubDeg
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nh; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = hroots[q];
+        if (off[r + 1] - off[r] <= kHubDeg) atomicMin(firstq, (unsigned long long)q);
+    }
+}
 __global__ void k_scatter_hbase(int64_t nh, const int32_t *__restrict__ hroots, const int64_t *__restrict__ seg,
                                 int64_t *__restrict__ hbase) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nh; q += (int64_t)gridDim.x * blockDim.x)
@@ -2417,6 +2433,21 @@ vdmc_status build_schedule(vdmc_graph *g, cudaStream_t s) {
         VDMC_LAUNCH();
         int64_t sumD = 0;
         VDMC_CUDA(cudaMemcpyAsync(&sumD, segs + nhr, sizeof sumD, cudaMemcpyDeviceToHost, s));
+        {   // hub prefix: heavy tasks of the leading roots of degree > kHubDeg (fetched in smaller chunks)
+            unsigned long long *firstq = nullptr;
+            VDMC_CUDA(dalloc((void **)&firstq, sizeof(unsigned long long), s));
+            const unsigned long long init = (unsigned long long)nhr;
+            VDMC_CUDA(cudaMemcpyAsync(firstq, &init, sizeof init, cudaMemcpyHostToDevice, s));
+            k_hub_prefix<<<148, 256, 0, s>>>(nhr, g->hroots, g->off, firstq);
+            VDMC_LAUNCH();
+            unsigned long long q = 0;
+            VDMC_CUDA(cudaMemcpyAsync(&q, firstq, sizeof q, cudaMemcpyDeviceToHost, s));
+            VDMC_CUDA(cudaStreamSynchronize(s));
+            int64_t ht = 0;
+            VDMC_CUDA(cudaMemcpy(&ht, segs + q, sizeof ht, cudaMemcpyDeviceToHost));
+            g->hub_tasks = ht;
+            dfree(firstq, s);
+        }
         VDMC_CUDA(cudaStreamSynchronize(s));
         dfree(ts, s);
         // counts -> offsets -> entries
@@ -2571,6 +2602,7 @@ static vdmc_status run(const vdmc_graph *g, const uint8_t *lut, const CountOpts 
     d.maxdeg = (int)g->max_degree;
     d.off32 = (uint64_t)std::max<int64_t>(g->n, 1) * C < (1ull << 32) ? 1 : 0;
     d.hbase = g->hbase;
+    d.hub_tasks = g->hub_tasks;
     d.nr_off = g->nr_off;
     d.nr_adj = g->nr_adj;
     // k = 4 closed form at heavy roots: the "2+1" R[j] side per root (k_rside) from the tasks' M

@@ -87,6 +87,7 @@ struct vdmc_graph {
     // entries of the position p of root r: nr_adj[nr_off[hbase[r] + p] .. nr_off[hbase[r] + p + 1])
     int32_t *hroots = nullptr;     // [nhroots] heavy roots, rank order
     int64_t nhroots = 0;
+    int64_t hub_tasks = 0;         // heavy tasks of the leading roots of degree > kHubDeg (enum.cu)
     int64_t *hbase = nullptr;      // [n] segment base per heavy root
     int64_t *nr_off = nullptr;     // [sum D+ over heavy roots + 1]
     uint32_t *nr_adj = nullptr;    // position << 2 | code(x, R[position])
